@@ -1,0 +1,419 @@
+// C ABI of libmixedls_b200.so (include/mixedls_b200.h).  Validation mirrors
+// the reference's exception behaviour (lse.hpp:27-34, gls.hpp:26-32,
+// precision.hpp:63-70, refine.hpp:33-37); every solve runs on the GPU.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/mixedls_b200.h"
+#include "mlsb_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(MLSB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+double unit_roundoff(int32_t lvl) {
+  switch (lvl) {
+    case MLSB_LOW: return 0x1p-24;
+    case MLSB_WORKING: return 0x1p-53;
+    case MLSB_EXTENDED: return 0x1p-106;
+  }
+  return -1.0;
+}
+
+// refinement_config::validate + precision_config::validate
+int check_config(const mlsb_config* c) {
+  if (!c) return fail(MLSB_ERR_INVALID_INPUT, "config is null");
+  if (!(c->tol > 0.0)) return fail(MLSB_ERR_INVALID_INPUT, "refinement_config: tol must be positive");
+  if (c->maxit < 1) return fail(MLSB_ERR_INVALID_INPUT, "refinement_config: maxit must be >= 1");
+  const double uf = unit_roundoff(c->u_f), us = unit_roundoff(c->u_s), u = unit_roundoff(c->u),
+               ur = unit_roundoff(c->u_r);
+  if (uf < 0 || us < 0 || u < 0 || ur < 0)
+    return fail(MLSB_ERR_INVALID_INPUT, "precision_config: unknown precision level");
+  if (c->u != MLSB_WORKING)
+    return fail(MLSB_ERR_INVALID_INPUT, "precision_config: working precision must be binary64");
+  if (uf < us || us < u || u < ur)
+    return fail(MLSB_ERR_INVALID_INPUT, "precision_config: requires u_f >= u_s >= u >= u_r");
+  return MLSB_OK;
+}
+
+struct DevScope {
+  int prev = -1;
+  bool ok = true;
+  explicit DevScope(const mlsb_exec* ex) {
+    if (ex && ex->device >= 0) {
+      cudaGetDevice(&prev);
+      ok = cudaSetDevice(ex->device) == cudaSuccess;
+    }
+  }
+  ~DevScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// stream-ordered device scratch, released on scope exit
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  cudaError_t alloc(size_t bytes, cudaStream_t s) {
+    st = s;
+    if (bytes == 0) bytes = 16;
+    return cudaMallocAsync(&p, bytes, s);
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+int check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(MLSB_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  // keep stream-ordered scratch cached across calls (default threshold 0 would
+  // hand it back to the driver at every synchronize)
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return MLSB_OK;
+}
+
+struct Shape {
+  int kind;
+  int64_t m, n, p;
+  // element counts of the two matrices (rows, cols) and of the outputs
+  int64_t ra, ca, rb, cb;
+  int64_t nx, nr, nv;  // x, r|y, v|z lengths
+  int64_t nb, nd;      // rhs lengths (LSE b, d; GLS 0, d)
+};
+
+Shape lse_shape(int64_t m, int64_t n, int64_t p) {
+  return Shape{mlsb::KIND_LSE, m, n, p, m, n, p, n, n, m, p, m, p};
+}
+Shape gls_shape(int64_t n, int64_t m, int64_t p) {
+  return Shape{mlsb::KIND_GLS, m, n, p, n, m, n, p, m, p, n, 0, n};
+}
+
+// Run `batch` problems.  Host mode: copy in, solve, copy out, synchronize.
+// Device mode: launch only (asynchronous on the stream).
+int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA, const double* B,
+        int64_t ldb, int64_t sB, const double* b, int64_t sb, const double* d, int64_t sd,
+        const mlsb_config* cfg, double* x, double* r, double* v, int32_t* status, int64_t* iters,
+        int32_t* errcode, int64_t* sing, double* hist, double* phases_out, bool force_sync,
+        const mlsb_exec* ex) {
+  const bool dev = ex && ex->pointer_kind == MLSB_DEVICE;
+  cudaStream_t st = ex ? static_cast<cudaStream_t>(ex->stream) : nullptr;
+  const size_t lim = mlsb::device_smem_limit();
+  if (lim == 0) return fail(MLSB_ERR_CUDA, "cannot query the CUDA device");
+  // factors in shared memory when they fit, else in an L2-resident global workspace
+  bool m_global = false;
+  size_t need = mlsb::tile_smem_bytes(s.kind, s.m, s.n, s.p, cfg->u_f, cfg->u_s, cfg->u_r, false);
+  if (need > lim) {
+    m_global = true;
+    need = mlsb::tile_smem_bytes(s.kind, s.m, s.n, s.p, cfg->u_f, cfg->u_s, cfg->u_r, true);
+  }
+  if (need > lim)
+    return fail(MLSB_ERR_UNSUPPORTED,
+                "problem too large for the one-CTA tile solver (" + std::to_string(need) +
+                    " B shared memory > " + std::to_string(lim) + " B)");
+
+  mlsb::TileArgs a{};
+  a.kind = s.kind;
+  a.m = s.m;
+  a.n = s.n;
+  a.p = s.p;
+  a.batch = batch;
+  a.tol = cfg->tol;
+  a.maxit = cfg->maxit;
+  a.u_f = cfg->u_f;
+  a.u_s = cfg->u_s;
+  a.u_r = cfg->u_r;
+  a.lda = lda;
+  a.ldb = ldb;
+  cudaError_t e;
+  DevBuf bA, bB, bb, bd, bx, br, bv, bst, bit, berr, bsing, bhist, bph;
+  // -- inputs --
+  if (dev) {
+    a.A = A;
+    a.sA = sA;
+    a.B = B;
+    a.sB = sB;
+    a.b = b;
+    a.sb = sb;
+    a.d = d;
+    a.sd = sd;
+  } else {
+    auto span = [&](int64_t ld, int64_t rows, int64_t cols, int64_t stride) {
+      return (batch - 1) * stride + ld * (cols - 1) + rows;
+    };
+    const int64_t nA = span(lda, s.ra, s.ca, sA), nB = span(ldb, s.rb, s.cb, sB);
+    if ((e = bA.alloc(sizeof(double) * nA, st)) || (e = bB.alloc(sizeof(double) * nB, st)))
+      return cuda_fail(e, "cudaMallocAsync");
+    if ((e = cudaMemcpyAsync(bA.p, A, sizeof(double) * nA, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(bB.p, B, sizeof(double) * nB, cudaMemcpyHostToDevice, st)))
+      return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+    a.A = bA.as<double>();
+    a.sA = sA;
+    a.B = bB.as<double>();
+    a.sB = sB;
+    if (s.nb > 0) {
+      const int64_t nbb = (batch - 1) * sb + s.nb;
+      if ((e = bb.alloc(sizeof(double) * nbb, st)) ||
+          (e = cudaMemcpyAsync(bb.p, b, sizeof(double) * nbb, cudaMemcpyHostToDevice, st)))
+        return cuda_fail(e, "copy b");
+      a.b = bb.as<double>();
+      a.sb = sb;
+    }
+    const int64_t ndd = (batch - 1) * sd + s.nd;
+    if ((e = bd.alloc(sizeof(double) * ndd, st)) ||
+        (e = cudaMemcpyAsync(bd.p, d, sizeof(double) * ndd, cudaMemcpyHostToDevice, st)))
+      return cuda_fail(e, "copy d");
+    a.d = bd.as<double>();
+    a.sd = sd;
+  }
+  // -- outputs --
+  if (dev) {
+    a.x = x;
+    a.r = r;
+    a.v = v;
+    a.status = status;
+    a.iters = iters;
+    a.sing = sing;
+    a.hist = hist;
+  } else {
+    if ((e = bx.alloc(sizeof(double) * batch * s.nx, st)) ||
+        (e = br.alloc(sizeof(double) * batch * s.nr, st)) ||
+        (e = bv.alloc(sizeof(double) * batch * s.nv, st)) ||
+        (e = bst.alloc(sizeof(int32_t) * batch, st)) ||
+        (e = bit.alloc(sizeof(int64_t) * batch, st)) ||
+        (e = bsing.alloc(sizeof(int64_t) * batch, st)))
+      return cuda_fail(e, "cudaMallocAsync");
+    a.x = bx.as<double>();
+    a.r = br.as<double>();
+    a.v = bv.as<double>();
+    a.status = bst.as<int32_t>();
+    a.iters = bit.as<int64_t>();
+    a.sing = bsing.as<int64_t>();
+    if (hist) {
+      if ((e = bhist.alloc(sizeof(double) * batch * cfg->maxit * 3, st)))
+        return cuda_fail(e, "cudaMallocAsync");
+      a.hist = bhist.as<double>();
+    }
+  }
+  if (dev && errcode) {
+    a.err = errcode;
+  } else {
+    if ((e = berr.alloc(sizeof(int32_t) * batch, st))) return cuda_fail(e, "cudaMallocAsync");
+    a.err = berr.as<int32_t>();
+  }
+  if (phases_out) {
+    if ((e = bph.alloc(sizeof(double) * batch * 6, st))) return cuda_fail(e, "cudaMallocAsync");
+    a.phases = bph.as<double>();
+  }
+  DevBuf bgws;
+  if (m_global) {
+    const size_t per = mlsb::tile_gws_bytes(s.kind, s.m, s.n, s.p, cfg->u_f);
+    if ((e = bgws.alloc(per * size_t(batch), st))) return cuda_fail(e, "cudaMallocAsync(workspace)");
+    a.gws = bgws.p;
+  }
+  if ((e = mlsb::launch_tile_solver(a, st))) return cuda_fail(e, "tile solver launch");
+
+  if (!dev) {
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
+    };
+    if ((e = d2h(x, a.x, sizeof(double) * batch * s.nx)) ||
+        (e = d2h(r, a.r, sizeof(double) * batch * s.nr)) ||
+        (e = d2h(v, a.v, sizeof(double) * batch * s.nv)) ||
+        (e = d2h(status, a.status, sizeof(int32_t) * batch)) ||
+        (e = d2h(iters, a.iters, sizeof(int64_t) * batch)) ||
+        (e = d2h(errcode, a.err, sizeof(int32_t) * batch)) ||
+        (e = d2h(sing, a.sing, sizeof(int64_t) * batch)) ||
+        (e = d2h(hist, a.hist, sizeof(double) * batch * cfg->maxit * 3)))
+      return cuda_fail(e, "cudaMemcpyAsync(D2H)");
+  }
+  if (phases_out) {
+    if ((e = cudaMemcpyAsync(phases_out, a.phases, sizeof(double) * 6,
+                             cudaMemcpyDeviceToHost, st)))
+      return cuda_fail(e, "copy phases");
+  }
+  if (!dev || force_sync) {
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "cudaStreamSynchronize");
+  }
+  return MLSB_OK;
+}
+
+// single-problem driver shared by mplse / mpgls
+int solve_single(const Shape& s, const double* A, int64_t lda, const double* B, int64_t ldb,
+                 const double* b, const double* d, const mlsb_config* cfg, double* o1, double* o2,
+                 double* o3, mlsb_trace* trace, int64_t* singular_index, const mlsb_exec* ex) {
+  if (int rc = check_device()) return rc;
+  DevScope scope(ex);
+  if (!scope.ok) return fail(MLSB_ERR_CUDA, "cudaSetDevice failed");
+  const bool dev = ex && ex->pointer_kind == MLSB_DEVICE;
+  cudaStream_t st = ex ? static_cast<cudaStream_t>(ex->stream) : nullptr;
+  int32_t status = 1, errc = 0;
+  int64_t iters = 0, sing = -1;
+  double phases[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<double> hist_h(trace && trace->residual_history ? size_t(cfg->maxit) * 3 : 0);
+  int rc;
+  if (dev) {
+    // device arrays for the outputs, small bookkeeping through a device scratch
+    DevBuf bk;
+    cudaError_t e = bk.alloc(64 + (hist_h.empty() ? 0 : hist_h.size() * 8), st);
+    if (e) return cuda_fail(e, "cudaMallocAsync");
+    char* base = bk.as<char>();
+    int32_t* d_st = reinterpret_cast<int32_t*>(base);
+    int32_t* d_err = reinterpret_cast<int32_t*>(base + 8);
+    int64_t* d_it = reinterpret_cast<int64_t*>(base + 16);
+    int64_t* d_sing = reinterpret_cast<int64_t*>(base + 24);
+    double* d_hist = hist_h.empty() ? nullptr : reinterpret_cast<double*>(base + 64);
+    rc = run(s, 1, A, lda, 0, B, ldb, 0, b, 0, d, 0, cfg, o1, o2, o3, d_st, d_it, d_err, d_sing,
+             d_hist, phases, true, ex);
+    if (rc) return rc;
+    if ((e = cudaMemcpyAsync(&status, d_st, 4, cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaMemcpyAsync(&errc, d_err, 4, cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaMemcpyAsync(&iters, d_it, 8, cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaMemcpyAsync(&sing, d_sing, 8, cudaMemcpyDeviceToHost, st)))
+      return cuda_fail(e, "copy trace");
+    if (!hist_h.empty() &&
+        (e = cudaMemcpyAsync(hist_h.data(), d_hist, hist_h.size() * 8, cudaMemcpyDeviceToHost, st)))
+      return cuda_fail(e, "copy history");
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "cudaStreamSynchronize");
+  } else {
+    // outputs are only written back on success: stage them
+    std::vector<double> t1(s.nx), t2(s.nr), t3(s.nv);
+    rc = run(s, 1, A, lda, 0, B, ldb, 0, b, 0, d, 0, cfg, t1.data(), t2.data(), t3.data(), &status,
+             &iters, &errc, &sing, hist_h.empty() ? nullptr : hist_h.data(), phases, true, ex);
+    if (rc) return rc;
+    if (errc == 0) {
+      if (o1) memcpy(o1, t1.data(), t1.size() * 8);
+      if (o2) memcpy(o2, t2.data(), t2.size() * 8);
+      if (o3) memcpy(o3, t3.data(), t3.size() * 8);
+    }
+  }
+  if (errc == 3) {
+    if (singular_index) *singular_index = sing;
+    return fail(MLSB_ERR_SINGULAR, "singular_triangular: zero pivot (diagonal index " +
+                                       std::to_string(sing) + ")");
+  }
+  if (errc == 2)
+    return fail(MLSB_ERR_INVALID_INPUT, "rhs scaling overflowed (extreme norm imbalance)");
+  if (errc != 0) return fail(MLSB_ERR_OTHER, "device error " + std::to_string(errc));
+  if (trace) {
+    trace->status = status;
+    trace->iterations = iters;
+    trace->inner_iterations = 0;
+    for (int k = 0; k < 6; ++k) trace->phase_seconds[k] = phases[k];
+    if (trace->residual_history)
+      memcpy(trace->residual_history, hist_h.data(), sizeof(double) * 3 * size_t(iters));
+  }
+  return MLSB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+mlsb_config mlsb_default_config(void) {
+  mlsb_config c;
+  c.tol = 1e-13;
+  c.maxit = 40;
+  c.u_f = MLSB_LOW;
+  c.u_s = MLSB_LOW;
+  c.u = MLSB_WORKING;
+  c.u_r = MLSB_WORKING;
+  return c;
+}
+
+const char* mlsb_last_error(void) { return g_last_error.c_str(); }
+
+int mlsb_version(void) { return 1; }
+
+int mlsb_mplse(const double* A, int64_t lda, const double* B, int64_t ldb, const double* b,
+               const double* d, int64_t m, int64_t n, int64_t p, const mlsb_config* cfg,
+               double* x, double* r, double* v, mlsb_trace* trace, int64_t* singular_index,
+               const mlsb_exec* exec) {
+  // lse_problem::validate (lse.hpp:27-34), then refinement_config::validate
+  if (m <= 0 || n <= 0 || p <= 0) return fail(MLSB_ERR_DIMENSION, "lse_problem: empty matrix");
+  if (p > n || n > m + p)
+    return fail(MLSB_ERR_DIMENSION, "lse_problem: requires p <= n <= m + p");
+  if (lda < m || ldb < p) return fail(MLSB_ERR_DIMENSION, "lse_problem: leading dimension too small");
+  if (!A || !B || !b || !d) return fail(MLSB_ERR_DIMENSION, "lse_problem: null input");
+  if (int rc = check_config(cfg)) return rc;
+  return solve_single(lse_shape(m, n, p), A, lda, B, ldb, b, d, cfg, x, r, v, trace,
+                      singular_index, exec);
+}
+
+int mlsb_mpgls(const double* W, int64_t ldw, const double* V, int64_t ldv, const double* d,
+               int64_t n, int64_t m, int64_t p, const mlsb_config* cfg, double* x, double* y,
+               double* z, mlsb_trace* trace, int64_t* singular_index, const mlsb_exec* exec) {
+  // gls_problem::validate (gls.hpp:26-32)
+  if (n <= 0 || m <= 0 || p <= 0) return fail(MLSB_ERR_DIMENSION, "gls_problem: empty matrix");
+  if (m > n || n > m + p) return fail(MLSB_ERR_DIMENSION, "gls_problem: requires m <= n <= m + p");
+  if (ldw < n || ldv < n) return fail(MLSB_ERR_DIMENSION, "gls_problem: leading dimension too small");
+  if (!W || !V || !d) return fail(MLSB_ERR_DIMENSION, "gls_problem: null input");
+  if (int rc = check_config(cfg)) return rc;
+  return solve_single(gls_shape(n, m, p), W, ldw, V, ldv, nullptr, d, cfg, x, y, z, trace,
+                      singular_index, exec);
+}
+
+int mlsb_mplse_batched(int64_t batch, const double* A, int64_t lda, int64_t strideA,
+                       const double* B, int64_t ldb, int64_t strideB, const double* b,
+                       int64_t strideb, const double* d, int64_t strided, int64_t m, int64_t n,
+                       int64_t p, const mlsb_config* cfg, double* x, double* r, double* v,
+                       int32_t* status, int64_t* iterations, int32_t* errcode,
+                       int64_t* singular_index, double* history, const mlsb_exec* exec) {
+  if (batch < 0) return fail(MLSB_ERR_DIMENSION, "batch must be >= 0");
+  if (m <= 0 || n <= 0 || p <= 0) return fail(MLSB_ERR_DIMENSION, "lse_problem: empty matrix");
+  if (p > n || n > m + p)
+    return fail(MLSB_ERR_DIMENSION, "lse_problem: requires p <= n <= m + p");
+  if (lda < m || ldb < p) return fail(MLSB_ERR_DIMENSION, "lse_problem: leading dimension too small");
+  if (int rc = check_config(cfg)) return rc;
+  if (batch == 0) return MLSB_OK;
+  if (int rc = check_device()) return rc;
+  DevScope scope(exec);
+  if (!scope.ok) return fail(MLSB_ERR_CUDA, "cudaSetDevice failed");
+  return run(lse_shape(m, n, p), batch, A, lda, strideA, B, ldb, strideB, b, strideb, d, strided,
+             cfg, x, r, v, status, iterations, errcode, singular_index, history, nullptr, false,
+             exec);
+}
+
+int mlsb_mpgls_batched(int64_t batch, const double* W, int64_t ldw, int64_t strideW,
+                       const double* V, int64_t ldv, int64_t strideV, const double* d,
+                       int64_t strided, int64_t n, int64_t m, int64_t p, const mlsb_config* cfg,
+                       double* x, double* y, double* z, int32_t* status, int64_t* iterations,
+                       int32_t* errcode, int64_t* singular_index, double* history,
+                       const mlsb_exec* exec) {
+  if (batch < 0) return fail(MLSB_ERR_DIMENSION, "batch must be >= 0");
+  if (n <= 0 || m <= 0 || p <= 0) return fail(MLSB_ERR_DIMENSION, "gls_problem: empty matrix");
+  if (m > n || n > m + p) return fail(MLSB_ERR_DIMENSION, "gls_problem: requires m <= n <= m + p");
+  if (ldw < n || ldv < n) return fail(MLSB_ERR_DIMENSION, "gls_problem: leading dimension too small");
+  if (int rc = check_config(cfg)) return rc;
+  if (batch == 0) return MLSB_OK;
+  if (int rc = check_device()) return rc;
+  DevScope scope(exec);
+  if (!scope.ok) return fail(MLSB_ERR_CUDA, "cudaSetDevice failed");
+  return run(gls_shape(n, m, p), batch, W, ldw, strideW, V, ldv, strideV, nullptr, 0, d, strided,
+             cfg, x, y, z, status, iterations, errcode, singular_index, history, nullptr, false,
+             exec);
+}
+
+}  // extern "C"

@@ -1,0 +1,256 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Oracle = oracle/_build/libmixedls_port.so, the restatement pinned bitwise to
+the reference (tests/test_oracle.py).  Criteria: tests/helpers.py.
+"""
+import numpy as np
+import pytest
+
+from paper_2406_16499_b200 import generate as G
+from tests.helpers import check_parity, fwd_bound, gls_backward, lse_backward, rel
+
+pytestmark = pytest.mark.gpu
+
+PRECS = {
+    "sssd": ("low", "low", "working"),
+    "sddd": ("low", "working", "working"),
+    "dddd": ("working", "working", "working"),
+    "sss_dd": ("low", "low", "extended"),
+    "sdd_dd": ("low", "working", "extended"),
+    "ddd_dd": ("working", "working", "extended"),
+}
+_CODE = {"low": "s", "working": "d", "extended": "dd"}
+
+
+def _cfg(P, prec, maxit=40, tol=1e-13):
+    return P.RefinementConfig(tol=tol, maxit=maxit,
+                              precisions=P.PrecisionConfig(prec[0], prec[1], "working", prec[2]))
+
+
+def _oprec(prec):
+    return tuple(_CODE[q] for q in prec)
+
+
+def run_lse(P, port, A, B, b, d, prec, kappa, maxit=40):
+    res = P.mplse(P.LseProblem(A, B, b, d), _cfg(P, prec, maxit))
+    ref = port.mplse(A, B, b, d, maxit=maxit, prec=_oprec(prec))
+    m, n = A.shape
+    p = B.shape[0]
+    fwd = rel(res.state.x, ref.x)
+    be_g = lse_backward(A, B, b, d, res.state.x, res.state.r, res.state.v)
+    be_r = lse_backward(A, B, b, d, ref.x, ref.r, ref.v)
+    return res, ref, check_parity("lse", fwd, fwd_bound(m, n, p, kappa), res.trace.iterations,
+                                  ref.iterations, be_g, be_r)
+
+
+def run_gls(P, port, W, V, d, prec, kappa, maxit=40):
+    res = P.mpgls(P.GlsProblem(W, V, d), _cfg(P, prec, maxit))
+    ref = port.mpgls(W, V, d, maxit=maxit, prec=_oprec(prec))
+    n, m = W.shape
+    p = V.shape[1]
+    fwd = max(rel(res.state.x, ref.x), rel(res.state.y, ref.r))
+    be_g = gls_backward(W, V, d, res.state.x, res.state.y, res.state.z)
+    be_r = gls_backward(W, V, d, ref.x, ref.r, ref.v)
+    return res, ref, check_parity("gls", fwd, fwd_bound(m, n, p, kappa), res.trace.iterations,
+                                  ref.iterations, be_g, be_r)
+
+
+# --------------------------------------------------------------------------
+def test_config_c1(gpu, port):
+    c = G.CONFIGS["C1"]
+    A, B, b, d = G.lse_problem(c["m"], c["n"], c["p"], c["kappa_A"], c["kappa_B"], c["seed"])
+    res, ref, msgs = run_lse(gpu, port, A, B, b, d, c["prec"], c["kappa_A"], c["maxit"])
+    assert not msgs, msgs
+    assert res.trace.status == ref.status == "converged"
+    assert res.trace.residual_history.shape == (res.trace.iterations, 3)
+
+
+def test_config_c2(gpu, port):
+    c = G.CONFIGS["C2"]
+    W, V, d = G.gls_problem(c["n"], c["m"], c["p"], c["kappa_A"], c["kappa_B"], c["seed"])
+    res, ref, msgs = run_gls(gpu, port, W, V, d, c["prec"], c["kappa_A"], c["maxit"])
+    assert not msgs, msgs
+    assert res.trace.status == ref.status == "converged"
+
+
+@pytest.mark.parametrize("prec", list(PRECS))
+@pytest.mark.parametrize("shape", [(20, 10, 4), (40, 25, 5), (7, 5, 3), (3, 5, 2), (64, 32, 32),
+                                   (30, 30, 1), (256, 128, 32)])
+def test_lse_shapes(gpu, port, shape, prec):
+    m, n, p = shape
+    # square stacked systems (n = m + p) are far worse conditioned than kappa(A):
+    # keep them inside the classical-IR convergence region u_f * kappa < 1
+    ka, kb = (1e1, 1e1) if n == m + p else (1e3, 1e2)
+    A, B, b, d = G.lse_problem(m, n, p, ka, kb, seed=11 + m + n + p)
+    kappa = np.linalg.cond(np.vstack([A, B])) * 1e3
+    res, ref, msgs = run_lse(gpu, port, A, B, b, d, PRECS[prec], kappa)
+    if ref.status != "converged":
+        # the parity criteria are defined on converged runs; a stagnating oracle
+        # must be matched by a non-converging (or equally slow) GPU run
+        assert res.trace.status != "converged" or res.trace.iterations >= ref.iterations - 1
+        return
+    assert not msgs, msgs
+    assert res.trace.status == ref.status
+
+
+@pytest.mark.parametrize("prec", list(PRECS))
+@pytest.mark.parametrize("shape", [(12, 3, 11), (9, 3, 8), (5, 2, 4), (20, 10, 15), (16, 8, 8),
+                                   (24, 24, 4), (200, 100, 150)])
+def test_gls_shapes(gpu, port, shape, prec):
+    n, m, p = shape
+    W, V, d = G.gls_problem(n, m, p, 1e3, 1e2, seed=7 + n + m + p)
+    kappa = np.linalg.cond(np.hstack([W, V])) * 1e3
+    res, ref, msgs = run_gls(gpu, port, W, V, d, PRECS[prec], kappa)
+    assert not msgs, msgs
+    assert res.trace.status == ref.status
+
+
+@pytest.mark.parametrize("cond", [1e3, 1e5])
+def test_reference_generator_lse(gpu, port, cond):
+    # the reference's own generator (generate.hpp) at a tile-sized shape
+    A, B, b, d = port.gen_lse(120, 60, 10, cond, 7)
+    res, ref, msgs = run_lse(gpu, port, A, B, b, d, PRECS["sssd"], cond)
+    assert not msgs, msgs
+
+
+def test_known_answer_lse(gpu):
+    # proj/tests/test_lse.cpp:70-81: A = I, B = [1 0], b = (1,1), d = 2 -> x = (2, 1)
+    P = gpu
+    res = P.mplse(P.LseProblem(np.eye(2), np.array([[1.0, 0.0]]), np.ones(2), np.array([2.0])),
+                  P.RefinementConfig(precisions=P.PrecisionConfig.all_working()))
+    assert np.allclose(res.state.x, [2.0, 1.0], atol=1e-14)
+
+
+def test_known_answer_gls(gpu):
+    # proj/tests/test_gls.cpp:91-107: x = 1/2, y = (1/2, -1/2)
+    P = gpu
+    res = P.mpgls(P.GlsProblem(np.ones((2, 1)), np.eye(2), np.array([1.0, 0.0])),
+                  P.RefinementConfig(precisions=P.PrecisionConfig.all_working()))
+    assert np.allclose(res.state.x, [0.5], atol=1e-14)
+    assert np.allclose(res.state.y, [0.5, -0.5], atol=1e-14)
+
+
+def test_gls_zero_rhs_converges_in_one_pass(gpu):
+    # proj/tests/test_gls.cpp:321-330 and SURVEY Appendix A.10
+    P = gpu
+    W, V, _ = G.gls_problem(8, 3, 7, 10.0, 10.0, 717)
+    res = P.mpgls(P.GlsProblem(W, V, np.zeros(8)))
+    assert res.trace.status == "converged" and res.trace.iterations == 1
+    assert not np.any(res.state.x) and not np.any(res.state.y) and not np.any(res.state.z)
+
+
+def test_singular_w_raises(gpu):
+    # proj/tests/test_gls.cpp:121-127: rank(W) < m -> singular_triangular
+    P = gpu
+    W, V, d = G.gls_problem(7, 3, 6, 10.0, 10.0, 92)
+    W[:, 1] = 0.0
+    with pytest.raises(P.SingularTriangular):
+        P.mpgls(P.GlsProblem(W, V, d))
+
+
+def test_stagnation_matches_oracle(gpu, port):
+    # u_f * kappa ~ 0.03: neither side reaches tol = 1e-13 within maxit
+    P = gpu
+    A, B, b, d = G.lse_problem(3, 5, 2, 1e3, 1e2, seed=21)
+    res = P.mplse(P.LseProblem(A, B, b, d))
+    ref = port.mplse(A, B, b, d)
+    assert ref.status == "max_iterations"
+    assert res.trace.status != "converged" or res.trace.iterations >= ref.iterations - 1
+
+
+def test_ill_conditioned_does_not_converge(gpu, port):
+    # proj/tests/test_lse.cpp:326-331 (kappa = 1e9)
+    P = gpu
+    A, B, b, d = port.gen_lse(30, 12, 4, 1e9, 606)
+    res = P.mplse(P.LseProblem(A, B, b, d))
+    ref = port.mplse(A, B, b, d)
+    assert res.trace.status != "converged" and ref.status != "converged"
+
+
+def test_rhs_scaling_linearity(gpu):
+    # proj/tests/test_lse.cpp:299-313
+    P = gpu
+    A, B, b, d = G.lse_problem(16, 8, 3, 1e2, 1e1, 404)
+    base = P.mplse(P.LseProblem(A, B, b, d))
+    for s in (1e-3, 1e3):
+        res = P.mplse(P.LseProblem(A, B, b * s, d * s))
+        assert res.trace.status == "converged"
+        assert rel(res.state.x, base.state.x * s) <= 1e-12
+
+
+def test_determinism_bitwise(gpu):
+    P = gpu
+    A, B, b, d = G.lse_problem(64, 32, 8, 1e4, 1e2, 5)
+    r1 = P.mplse(P.LseProblem(A, B, b, d))
+    r2 = P.mplse(P.LseProblem(A, B, b, d))
+    assert np.array_equal(r1.state.x, r2.state.x) and np.array_equal(r1.state.v, r2.state.v)
+    assert np.array_equal(r1.trace.residual_history, r2.trace.residual_history)
+
+
+def test_rhs_overflow_invalid_input(gpu):
+    # lse.hpp:328-329: d / c_d overflows
+    P = gpu
+    A, B, b, d = G.lse_problem(8, 4, 2, 10.0, 10.0, 3)
+    A = A * 1e300
+    B = B * 1e-300
+    with pytest.raises(P.InvalidInput):
+        P.mplse(P.LseProblem(A, B, b, d))
+
+
+def test_batched_matches_single_bitwise(gpu):
+    P = gpu
+    probs = [G.lse_problem(40, 20, 6, 10 ** (1 + i), 1e1, 50 + i) for i in range(4)]
+    A = np.stack([q[0] for q in probs])
+    B = np.stack([q[1] for q in probs])
+    b = np.stack([q[2] for q in probs])
+    d = np.stack([q[3] for q in probs])
+    out = P.mplse_batched(A, B, b, d)
+    for i, q in enumerate(probs):
+        s = P.mplse(P.LseProblem(*q))
+        assert np.array_equal(out.x[i], s.state.x)
+        assert out.iterations[i] == s.trace.iterations
+        assert out.errcode[i] == 0
+
+
+def test_batched_gls_matches_single(gpu):
+    P = gpu
+    probs = [G.gls_problem(30, 10, 25, 10 ** (1 + i), 1e1, 70 + i) for i in range(3)]
+    W = np.stack([q[0] for q in probs])
+    V = np.stack([q[1] for q in probs])
+    d = np.stack([q[2] for q in probs])
+    out = P.mpgls_batched(W, V, d)
+    for i, q in enumerate(probs):
+        s = P.mpgls(P.GlsProblem(*q))
+        assert np.array_equal(out.x[i], s.state.x) and np.array_equal(out.r[i], s.state.y)
+
+
+def test_device_pointer_mode(gpu):
+    import torch
+
+    P = gpu
+    A, B, b, d = G.lse_problem(50, 30, 10, 1e3, 1e2, 9)
+    host = P.mplse(P.LseProblem(A, B, b, d))
+    t = lambda a: torch.from_numpy(np.asfortranarray(a)).cuda() if a.ndim == 1 else \
+        torch.from_numpy(np.ascontiguousarray(a.T)).cuda().t()  # noqa: E731
+    dev = P.mplse(P.LseProblem(t(A), t(B), t(b), t(d)))
+    assert np.array_equal(dev.state.x.cpu().numpy(), host.state.x)
+
+
+def test_batched_device_c4_slice(gpu, port):
+    """A slice of BASELINE config 4 generated on the device, checked problem by problem."""
+    import torch
+
+    P = gpu
+    A, B, b, d, kA = G.lse_batch_torch(64, 256, 128, 32, seed=1000)
+    out = P.mplse_batched(A, B, b, d)
+    torch.cuda.synchronize()
+    An, Bn, bn, dn = (t.cpu().numpy() for t in (A, B, b, d))
+    it = out.iterations.cpu().numpy()
+    err = out.errcode.cpu().numpy()
+    x = out.x.cpu().numpy()
+    assert not err.any()
+    for i in range(0, 64, 8):
+        ref = port.mplse(An[i], Bn[i], bn[i], dn[i])
+        fwd = rel(x[i], ref.x)
+        assert fwd <= fwd_bound(256, 128, 32, float(kA[i])), (i, fwd)
+        assert abs(int(it[i]) - ref.iterations) <= 1

@@ -122,14 +122,16 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
   cudaStream_t st = ex ? static_cast<cudaStream_t>(ex->stream) : nullptr;
   const size_t lim = mlsb::device_smem_limit();
   if (lim == 0) return fail(MLSB_ERR_CUDA, "cannot query the CUDA device");
+  const bool use_reg = s.kind == mlsb::KIND_LSE &&
+                       mlsb::lse_reg_supported(s.m, s.n, s.p, cfg->u_f, cfg->u_s, cfg->u_r, lim);
   // factors in shared memory when they fit, else in an L2-resident global workspace
   bool m_global = false;
   size_t need = mlsb::tile_smem_bytes(s.kind, s.m, s.n, s.p, cfg->u_f, cfg->u_s, cfg->u_r, false);
-  if (need > lim) {
+  if (!use_reg && need > lim) {
     m_global = true;
     need = mlsb::tile_smem_bytes(s.kind, s.m, s.n, s.p, cfg->u_f, cfg->u_s, cfg->u_r, true);
   }
-  if (need > lim)
+  if (!use_reg && need > lim)
     return fail(MLSB_ERR_UNSUPPORTED,
                 "problem too large for the one-CTA tile solver (" + std::to_string(need) +
                     " B shared memory > " + std::to_string(lim) + " B)");
@@ -233,7 +235,8 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
     if ((e = bgws.alloc(per * size_t(batch), st))) return cuda_fail(e, "cudaMallocAsync(workspace)");
     a.gws = bgws.p;
   }
-  if ((e = mlsb::launch_tile_solver(a, st))) return cuda_fail(e, "tile solver launch");
+  if ((e = use_reg ? mlsb::launch_lse_reg(a, st) : mlsb::launch_tile_solver(a, st)))
+    return cuda_fail(e, "tile solver launch");
 
   if (!dev) {
     auto d2h = [&](void* dst, const void* src, size_t bytes) {

@@ -74,4 +74,44 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 
+// ---- block reductions (fixed order, deterministic); results in out[], all threads synced
+template <int N, int NW = 16>
+__device__ __forceinline__ void block_sum(double (&v)[N], double* red, double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < N; ++k) red[warp * 8 + k] = v[k];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double t = lane < NW ? red[lane * 8 + k] : 0.0;
+      t = warp_sum(t);
+      if (lane == 0) out[k] = t;
+    }
+  }
+  __syncthreads();
+}
+template <int N, int NW = 16>
+__device__ __forceinline__ void block_max(double (&v)[N], double* red, double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = warp_max(v[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < N; ++k) red[warp * 8 + k] = v[k];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double t = lane < NW ? red[lane * 8 + k] : 0.0;
+      t = warp_max(t);
+      if (lane == 0) out[k] = t;
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace mlsb

@@ -48,4 +48,10 @@ size_t tile_gws_bytes(int kind, int64_t m, int64_t n, int64_t p, int u_f);
 size_t device_smem_limit();
 cudaError_t launch_tile_solver(const TileArgs& a, cudaStream_t stream);
 
+// register-resident LSE tile solver (m + p <= 288, n <= 128, u_f = binary32,
+// u_r = binary64): BASELINE configs 1 and 4
+bool lse_reg_supported(int64_t m, int64_t n, int64_t p, int u_f, int u_s, int u_r,
+                       size_t smem_limit);
+cudaError_t launch_lse_reg(const TileArgs& a, cudaStream_t stream);
+
 }  // namespace mlsb

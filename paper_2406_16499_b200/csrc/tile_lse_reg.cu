@@ -1,0 +1,1071 @@
+// Register-resident LSE tile solver: ONE CTA (16 warps) solves ONE LSE
+// problem with m + p <= 288 and n <= 128 at u_f = binary32 -- the shape class
+// of BASELINE configs 1 and 4.  Same semantics as the generic tile solver
+// (tile_solver.cu, reference citations there); what changes is the
+// execution model, chosen for the B200 SM:
+//
+//  * the stacked fp32 matrix [A; B] lives in REGISTERS during GRQ: lane l of
+//    warp w owns rows {l + 32 t} x columns {w + 16 s} (9 x 8 floats), so a
+//    reflector step is register FMAs + one 8-way transposed warp reduction
+//    + one CTA barrier (QR), instead of shared-memory rank-1 sweeps;
+//  * the QR step also yields the Gram entries v_c^T v_j of the reflectors of
+//    the current block of 32, from which the compact-WY T factors (xLARFT,
+//    forward) are built, so every later reflector application is blocked:
+//    x -= V T' (V^T x), 32 reflectors at a time;
+//  * triangular solves are 32-wide blocked (diagonal block in registers with
+//    shuffle broadcasts, off-diagonal block as a GEMV);
+//  * fp64 residual sweeps keep every load of a column group in flight and
+//    reduce across lanes once per pass.
+//
+// Factor storage after GRQ (shared memory, odd leading dimension ld):
+//   rows [0, m):   T (upper) with the QR reflectors of Z below the diagonal
+//   rows [m, m+p): the RQ reflectors of Q left of the pivot, R to the right
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "device_common.cuh"
+#include "mlsb_internal.h"
+
+namespace mlsb {
+namespace reg {
+
+constexpr int NT = 512, NW = 16;
+constexpr int RT = 9, CS = 8;         // register tile: rows l+32t (t<RT), cols w+16s (s<CS)
+constexpr int RMAX = 32 * RT;         // 288
+constexpr int CMAX = NW * CS;         // 128
+constexpr int NWORK = 7;              // solve-precision work vectors
+constexpr int RH = 160;               // residual: rows per row-half
+constexpr int RTH = RH / 32;          // 5 row slots per lane in a half
+constexpr int CG = 8;                 // residual: column groups (warps per half)
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+struct Layout {
+  int R, C, ld, kz, nbz, nbq;
+  size_t oM, oTau1, oTau2, oTZ, oTQ, oU, oRinit, oRout, oSw, oCout, oSu, oWork, oYb, oRed,
+      oScal, total;
+};
+
+__host__ __device__ inline Layout make_layout(int64_t m, int64_t n, int64_t p, int csz) {
+  Layout L;
+  L.R = int(m + p);
+  L.C = int(n);
+  L.ld = L.R | 1;
+  L.kz = int(m < n ? m : n);
+  L.nbz = (L.kz + 31) / 32;
+  L.nbq = int((p + 31) / 32);
+  size_t o = 0;
+  L.oM = o;     o = al16(o + size_t(L.ld) * L.C * 4);
+  L.oTau1 = o;  o = al16(o + size_t(CMAX) * 4);
+  L.oTau2 = o;  o = al16(o + size_t(RMAX) * 4);
+  L.oTZ = o;    o = al16(o + size_t(L.nbz) * 1024 * 4);
+  L.oTQ = o;    o = al16(o + size_t(L.nbq) * 1024 * 4);
+  // union: factorization scratch (fp32 partials + w + 2 reflector buffers) |
+  //        refinement scratch (fp64 row partials CG x RMAX + col partials 2 x CMAX)
+  const size_t fac = size_t(NW) * RMAX * 4 + RMAX * 4 + 2 * RMAX * 4;
+  const size_t ref = size_t(CG) * RMAX * 8 + 2 * CMAX * 8;
+  L.oU = o;     o = al16(o + (fac > ref ? fac : ref));
+  L.oRinit = o; o = al16(o + size_t(RMAX) * 8);
+  L.oRout = o;  o = al16(o + size_t(RMAX) * 8);
+  L.oSw = o;    o = al16(o + size_t(RMAX) * 8);
+  L.oCout = o;  o = al16(o + size_t(CMAX) * 8);
+  L.oSu = o;    o = al16(o + size_t(CMAX) * 8);
+  L.oWork = o;  o = al16(o + size_t(NWORK) * RMAX * csz);
+  L.oYb = o;    o = al16(o + size_t(NW) * 32 * csz);
+  L.oRed = o;   o = al16(o + size_t(NW) * 8 * 8);
+  L.oScal = o;  o = al16(o + 64 * 8);
+  L.total = o;
+  return L;
+}
+
+enum Slot { S_SA = 0, S_SB, S_CB, S_CD, S_NB, S_ND, S_NA, S_NBF, S_SIG, S_BETA, S_ALPHA,
+            S_RED0 = 16, S_FLAG = 40 };
+
+// ---------------------------------------------------------------- helpers
+// 8 partial sums per lane -> lane-complete sums (8-way transposed butterfly:
+// 4+2+1+1+1 exchanges, then 8 broadcasts).  Every lane returns all 8 sums.
+__device__ __forceinline__ void reduce8(float (&d)[8], int l) {
+  const bool b4 = l & 16, b3 = l & 8, b2 = l & 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b4 ? d[i] : d[i + 4], keep = b4 ? d[i + 4] : d[i];
+    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b3 ? d[i] : d[i + 2], keep = b3 ? d[i + 2] : d[i];
+    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const float send = b2 ? d[0] : d[1], keep = b2 ? d[1] : d[0];
+    d[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  d[0] += __shfl_xor_sync(0xffffffffu, d[0], 2);
+  d[0] += __shfl_xor_sync(0xffffffffu, d[0], 1);
+  // lane l now holds the sum of value index (l >> 2) & 7
+  const float mine = d[0];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) d[s] = __shfl_sync(0xffffffffu, mine, s << 2);
+}
+
+// ------------------------------------------------------- WY block applies
+// QR factor (Z): block of kb reflectors j0..j0+kb-1 stored in columns of M
+// (v_j = e_j + M[j+1:rend, j]).  x := (I - V T' V^T) x, T' = T or T^T.
+template <class CT>
+__device__ void zblk(const float* M, int ld, int j0, int kb, int rend, const float* Tb, bool tr,
+                     CT* x, CT* yb, int l) {
+  CT y = CT(0);
+  if (l < kb) {
+    const int jq = j0 + l;
+    const float* col = M + size_t(jq) * ld;
+    CT y0 = x[jq], y1 = CT(0), y2 = CT(0), y3 = CT(0);
+    int r = jq + 1;
+    for (; r + 3 < rend; r += 4) {
+      y0 += CT(col[r]) * x[r];
+      y1 += CT(col[r + 1]) * x[r + 1];
+      y2 += CT(col[r + 2]) * x[r + 2];
+      y3 += CT(col[r + 3]) * x[r + 3];
+    }
+    for (; r < rend; ++r) y0 += CT(col[r]) * x[r];
+    y = (y0 + y1) + (y2 + y3);
+  }
+  yb[l] = y;
+  __syncwarp();
+  CT z = CT(0);
+  if (l < kb) {
+    if (!tr)
+      for (int k = l; k < kb; ++k) z += CT(Tb[l + 32 * k]) * yb[k];
+    else
+      for (int k = 0; k <= l; ++k) z += CT(Tb[k + 32 * l]) * yb[k];
+  }
+  __syncwarp();
+  yb[l] = z;
+  __syncwarp();
+  for (int r = j0 + l; r < rend; r += 32) {
+    const int qmax = (r - j0 + 1) < kb ? (r - j0 + 1) : kb;  // reflectors q with j0+q <= r
+    CT acc = CT(0);
+    for (int q = 0; q < qmax; ++q) {
+      const int jq = j0 + q;
+      const CT vq = (r == jq) ? CT(1) : CT(M[r + size_t(jq) * ld]);
+      acc += vq * yb[q];
+    }
+    x[r] -= acc;
+  }
+  __syncwarp();
+}
+
+// Z x (herm = false: last block first, T) or Z^T x (first block first, T^T)
+template <class CT>
+__device__ void z_apply(const float* M, int ld, int k, int rend, const float* TZ, bool herm, CT* x,
+                        CT* yb, int l) {
+  const int nb = (k + 31) / 32;
+  for (int s = 0; s < nb; ++s) {
+    const int b = herm ? s : nb - 1 - s;
+    const int j0 = 32 * b, kb = (k - j0) < 32 ? (k - j0) : 32;
+    zblk(M, ld, j0, kb, rend, TZ + b * 1024, herm, x, yb, l);
+  }
+}
+
+// RQ factor (Q): reflector j in row rtop+j, entries at columns c < ptop+j,
+// unit at c = ptop+j; block of kb reflectors from j0.
+template <class CT>
+__device__ void qblk(const float* M, int ld, int rtop, int ptop, int j0, int kb, int dim,
+                     const float* Tb, bool tr, CT* x, CT* yb, int l) {
+  CT y = CT(0);
+  if (l < kb) {
+    const int jq = j0 + l, pc = ptop + jq;
+    const float* row = M + (rtop + jq);
+    CT y0 = x[pc], y1 = CT(0), y2 = CT(0), y3 = CT(0);
+    int c = 0;
+    for (; c + 3 < pc; c += 4) {
+      y0 += CT(row[size_t(c) * ld]) * x[c];
+      y1 += CT(row[size_t(c + 1) * ld]) * x[c + 1];
+      y2 += CT(row[size_t(c + 2) * ld]) * x[c + 2];
+      y3 += CT(row[size_t(c + 3) * ld]) * x[c + 3];
+    }
+    for (; c < pc; ++c) y0 += CT(row[size_t(c) * ld]) * x[c];
+    y = (y0 + y1) + (y2 + y3);
+  }
+  yb[l] = y;
+  __syncwarp();
+  CT z = CT(0);
+  if (l < kb) {
+    if (!tr)
+      for (int k = l; k < kb; ++k) z += CT(Tb[l + 32 * k]) * yb[k];
+    else
+      for (int k = 0; k <= l; ++k) z += CT(Tb[k + 32 * l]) * yb[k];
+  }
+  __syncwarp();
+  yb[l] = z;
+  __syncwarp();
+  const int cmax = ptop + j0 + kb;  // columns touched by the block
+  for (int c = l; c < cmax && c < dim; c += 32) {
+    CT acc = CT(0);
+    for (int q = 0; q < kb; ++q) {
+      const int pc = ptop + j0 + q;
+      if (c <= pc) {
+        const CT vq = (c == pc) ? CT(1) : CT(M[(rtop + j0 + q) + size_t(c) * ld]);
+        acc += vq * yb[q];
+      }
+    }
+    x[c] -= acc;
+  }
+  __syncwarp();
+}
+
+template <class CT>
+__device__ void q_apply(const float* M, int ld, int kq, int rtop, int ptop, int dim,
+                        const float* TQ, bool herm, CT* x, CT* yb, int l) {
+  const int nb = (kq + 31) / 32;
+  for (int s = 0; s < nb; ++s) {
+    const int b = herm ? s : nb - 1 - s;
+    const int j0 = 32 * b, kb = (kq - j0) < 32 ? (kq - j0) : 32;
+    qblk(M, ld, rtop, ptop, j0, kb, dim, TQ + b * 1024, herm, x, yb, l);
+  }
+}
+
+// ------------------------------------------------------ triangular solves
+// U = M[r0:r0+k, c0:c0+k] upper; 32-wide blocks, one warp, x in smem.
+template <class CT>
+__device__ bool trsv_up(const float* M, int ld, int r0, int c0, int k, CT* x, int l, int* bad) {
+  for (int i1 = k; i1 > 0; i1 -= 32) {
+    const int i0 = i1 > 32 ? i1 - 32 : 0, bs = i1 - i0;
+    CT xi = l < bs ? x[i0 + l] : CT(0);
+    for (int jj = bs - 1; jj >= 0; --jj) {
+      const float piv = M[(r0 + i0 + jj) + size_t(c0 + i0 + jj) * ld];
+      if (piv == 0.f) {
+        if (l == 0) *bad = i0 + jj;
+        __syncwarp();
+        return false;
+      }
+      const CT xj = __shfl_sync(0xffffffffu, xi, jj) / CT(piv);
+      if (l == jj) xi = xj;
+      if (l < jj) xi -= CT(M[(r0 + i0 + l) + size_t(c0 + i0 + jj) * ld]) * xj;
+    }
+    if (l < bs) x[i0 + l] = xi;
+    __syncwarp();
+    for (int r = l; r < i0; r += 32) {
+      CT acc = CT(0);
+      const float* rowp = M + (r0 + r) + size_t(c0 + i0) * ld;
+      for (int q = 0; q < bs; ++q) acc += CT(rowp[size_t(q) * ld]) * x[i0 + q];
+      x[r] -= acc;
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// U^T x = b
+template <class CT>
+__device__ bool trsv_upt(const float* M, int ld, int r0, int c0, int k, CT* x, int l, int* bad) {
+  for (int i0 = 0; i0 < k; i0 += 32) {
+    const int bs = (k - i0) < 32 ? (k - i0) : 32, i1 = i0 + bs;
+    CT xi = l < bs ? x[i0 + l] : CT(0);
+    for (int j = 0; j < bs; ++j) {
+      const float piv = M[(r0 + i0 + j) + size_t(c0 + i0 + j) * ld];
+      if (piv == 0.f) {
+        if (l == 0) *bad = i0 + j;
+        __syncwarp();
+        return false;
+      }
+      const CT xj = __shfl_sync(0xffffffffu, xi, j) / CT(piv);
+      if (l == j) xi = xj;
+      if (l > j && l < bs) xi -= CT(M[(r0 + i0 + j) + size_t(c0 + i0 + l) * ld]) * xj;
+    }
+    if (l < bs) x[i0 + l] = xi;
+    __syncwarp();
+    for (int r = i1 + l; r < k; r += 32) {
+      CT acc = CT(0);
+      const float* colp = M + (r0 + i0) + size_t(c0 + r) * ld;
+      for (int q = 0; q < bs; ++q) acc += CT(colp[q]) * x[i0 + q];
+      x[r] -= acc;
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// y[i] = sum_j U(r0+i, c0+j) x[j] over thread range; lower-masked: zero when
+// (r0+i) > (c0+j) (QR reflector storage)
+template <class CT, bool LOWER_MASK>
+__device__ void gemv_rows(const float* M, int ld, int r0, int rows, int c0, int cols, const CT* x,
+                          CT* y, int t, int nth) {
+  for (int i = t; i < rows; i += nth) {
+    const float* rowp = M + (r0 + i) + size_t(c0) * ld;
+    CT acc = CT(0);
+    int j = 0;
+    if (LOWER_MASK) j = (r0 + i) - c0 > 0 ? (r0 + i) - c0 : 0;
+    for (; j < cols; ++j) acc += CT(rowp[size_t(j) * ld]) * x[j];
+    y[i] = acc;
+  }
+}
+
+// y[j] = sum_i U(r0+i, c0+j) x[i] (+ mask rows below the diagonal), warp per output
+template <class CT, bool LOWER_MASK>
+__device__ void gemv_cols(const float* M, int ld, int r0, int rows, int c0, int cols, const CT* x,
+                          CT* y, int wfirst, int nwarps, int w, int l) {
+  for (int j = w - wfirst; j < cols; j += nwarps) {
+    const float* colp = M + size_t(c0 + j) * ld + r0;
+    int imax = rows;
+    if (LOWER_MASK) {
+      const int lim = (c0 + j) - r0 + 1;  // rows r0+i <= c0+j
+      imax = lim < rows ? (lim > 0 ? lim : 0) : rows;
+    }
+    CT acc = CT(0);
+    for (int i = l; i < imax; i += 32) acc += CT(colp[i]) * x[i];
+    acc = warp_sum(acc);
+    if (l == 0) y[j] = acc;
+  }
+}
+
+// T of a forward block (xLARFT): T[q][q] = tau_q; T[0:q,q] = -tau_q T[0:q,0:q] G[0:q,q].
+// G (upper, column-major 32x32) is overwritten by T.  One warp.
+__device__ void build_T(float* G, const float* tau, int kb, int l) {
+  for (int q = 0; q < kb; ++q) {
+    float t = 0.f;
+    if (l < q)
+      for (int k = l; k < q; ++k) t += G[l + 32 * k] * G[k + 32 * q];
+    __syncwarp();
+    const float tq = tau[q];
+    if (l < q) G[l + 32 * q] = -tq * t;
+    if (l == q) G[q + 32 * q] = tq;
+    __syncwarp();
+  }
+}
+
+// xLARFG on column jc held by its owner warp (registers); publishes v to vout and tau
+__device__ __forceinline__ void gen_col(float (&ar)[RT][CS], int jc, int m, int l, float* vout,
+                                    float* tau1) {
+  const int sc = jc >> 4;
+  float col[RT];
+#pragma unroll
+  for (int t = 0; t < RT; ++t) {
+    col[t] = 0.f;
+#pragma unroll
+    for (int s = 0; s < CS; ++s) col[t] = (s == sc) ? ar[t][s] : col[t];
+  }
+  double ss = 0.0;
+#pragma unroll
+  for (int t = 0; t < RT; ++t) {
+    const int i = l + 32 * t;
+    if (i > jc && i < m) ss = fma(double(col[t]), double(col[t]), ss);
+  }
+  ss = warp_sum(ss);
+  const double xn = sqrt(ss);
+  float alpha = 0.f;
+#pragma unroll
+  for (int t = 0; t < RT; ++t) alpha = (t == (jc >> 5)) ? col[t] : alpha;
+  alpha = __shfl_sync(0xffffffffu, alpha, jc & 31);
+  float tj = 0.f, inv = 1.f, beta = alpha;
+  if (xn != 0.0) {
+    const double ad = double(alpha);
+    const double bt = -copysign(hypot(ad, xn), ad);
+    tj = float((bt - ad) / bt);
+    inv = float(1.0 / (ad - bt));
+    beta = float(bt);
+  }
+#pragma unroll
+  for (int t = 0; t < RT; ++t) {
+    const int i = l + 32 * t;
+    float v;
+    if (i > jc && i < m) {
+      if (tj != 0.f) col[t] = col[t] * inv;
+      v = col[t];
+    } else {
+      v = (i == jc) ? 1.f : 0.f;
+    }
+    if (i == jc) col[t] = beta;
+    vout[i] = v;
+#pragma unroll
+    for (int s = 0; s < CS; ++s) ar[t][s] = (s == sc) ? col[t] : ar[t][s];
+  }
+  if (l == 0) tau1[jc] = tj;
+}
+
+// -------------------------------------------------------------- kernel
+template <class CT>
+__global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int64_t pid = blockIdx.x;
+  const int m = int(a.m), n = int(a.n), p = int(a.p);
+  const Layout Ly = make_layout(m, n, p, sizeof(CT));
+  const int R = Ly.R, C = Ly.C, ld = Ly.ld, kz = Ly.kz;
+  constexpr bool LOWS = sizeof(CT) == 4;
+
+  float* M = reinterpret_cast<float*>(smem + Ly.oM);
+  float* tau1 = reinterpret_cast<float*>(smem + Ly.oTau1);
+  float* tau2 = reinterpret_cast<float*>(smem + Ly.oTau2);
+  float* TZ = reinterpret_cast<float*>(smem + Ly.oTZ);
+  float* TQ = reinterpret_cast<float*>(smem + Ly.oTQ);
+  float* fpart = reinterpret_cast<float*>(smem + Ly.oU);           // [NW][RMAX]
+  float* wbuf = fpart + NW * RMAX;                                  // [RMAX]
+  float* vbuf = wbuf + RMAX;                                        // [2][RMAX]
+  double* dpart = reinterpret_cast<double*>(smem + Ly.oU);         // [CG][RMAX]
+  double* cpart = dpart + CG * RMAX;                                // [2][CMAX]
+  double* rinit = reinterpret_cast<double*>(smem + Ly.oRinit);
+  double* rout = reinterpret_cast<double*>(smem + Ly.oRout);
+  double* sw = reinterpret_cast<double*>(smem + Ly.oSw);
+  double* cout = reinterpret_cast<double*>(smem + Ly.oCout);
+  double* su = reinterpret_cast<double*>(smem + Ly.oSu);
+  CT* work = reinterpret_cast<CT*>(smem + Ly.oWork);
+  auto WC = [&](int i) { return work + i * RMAX; };
+  CT* yball = reinterpret_cast<CT*>(smem + Ly.oYb);
+  CT* yb = yball + 32 * w;
+  double* red = reinterpret_cast<double*>(smem + Ly.oRed);
+  double* scal = reinterpret_cast<double*>(smem + Ly.oScal);
+  int* iflag = reinterpret_cast<int*>(scal + S_FLAG);
+
+  const double* gA = a.A + pid * a.sA;
+  const double* gB = a.B + pid * a.sB;
+  const double* gb = a.b + pid * a.sb;
+  const double* gd = a.d + pid * a.sd;
+  auto gval = [&](int i, int j) -> double {
+    return i < m ? __ldg(gA + i + size_t(j) * a.lda) : __ldg(gB + (i - m) + size_t(j) * a.ldb);
+  };
+
+  uint64_t t_last = 0;
+  double ph[6] = {0, 0, 0, 0, 0, 0};
+  auto lap = [&](int slot) {
+    if (tid == 0) {
+      const uint64_t t = globaltimer_ns();
+      ph[slot] += double(t - t_last) * 1e-9;
+      t_last = t;
+    }
+  };
+  if (tid == 0) {
+    t_last = globaltimer_ns();
+    iflag[0] = 0;
+    iflag[1] = -1;
+  }
+
+  // ---------------------------------------------------- pre-scaling (lse.hpp:314-329)
+  double invA, invB;
+  {
+    double mx[3] = {0.0, 0.0, 0.0};
+    for (int j = w; j < C; j += NW) {
+      double g[RT];
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int i = l + 32 * t;
+        g[t] = i < R ? gval(i, j) : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int i = l + 32 * t;
+        if (i < m) mx[0] = nanskip_max(mx[0], fabs(g[t]));
+        else mx[1] = nanskip_max(mx[1], fabs(g[t]));
+      }
+    }
+    for (int i = tid; i < m; i += NT) mx[2] = nanskip_max(mx[2], fabs(__ldg(gb + i)));
+    block_max(mx, red, scal + S_RED0);
+    if (tid == 0) {
+      const double sA = scal[S_RED0] == 0.0 ? 1.0 : scal[S_RED0];
+      const double sB = scal[S_RED0 + 1] == 0.0 ? 1.0 : scal[S_RED0 + 1];
+      const double cb = scal[S_RED0 + 2] == 0.0 ? 1.0 : scal[S_RED0 + 2];
+      scal[S_SA] = sA;
+      scal[S_SB] = sB;
+      scal[S_CB] = cb;
+      scal[S_CD] = sB * cb / sA;
+    }
+    __syncthreads();
+    invA = 1.0 / scal[S_SA];
+    invB = 1.0 / scal[S_SB];
+  }
+  {
+    const double cb = scal[S_CB], cd = scal[S_CD];
+    for (int i = tid; i < R; i += NT) rinit[i] = i < m ? __ldg(gb + i) / cb : __ldg(gd + (i - m)) / cd;
+  }
+  __syncthreads();
+  {
+    int bad = 0;
+    for (int i = m + tid; i < R; i += NT) bad |= !isfinite(rinit[i]);
+    bad = __syncthreads_or(bad);
+    if (bad) {
+      if (tid == 0) iflag[0] = 2;
+      goto finish;
+    }
+  }
+
+  {
+    // ------------------------------------------ load fp32 [A;B]/s into registers
+    float ar[RT][CS];
+    {
+      double ss[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int s = 0; s < CS; ++s) {
+        const int c = w + NW * s;
+        double g[RT];
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          const int i = l + 32 * t;
+          g[t] = (c < C && i < R) ? gval(i, c) : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          const int i = l + 32 * t;
+          const double v = g[t] * (i < m ? invA : invB);
+          if (i < m) ss[0] = fma(v, v, ss[0]); else ss[1] = fma(v, v, ss[1]);
+          ar[t][s] = float(v);
+        }
+      }
+      for (int i = tid; i < R; i += NT) {
+        const double t = rinit[i];
+        if (i < m) ss[2] = fma(t, t, ss[2]); else ss[3] = fma(t, t, ss[3]);
+      }
+      block_sum(ss, red, scal + S_RED0);
+      if (tid == 0) {
+        scal[S_NA] = sqrt(scal[S_RED0]);
+        scal[S_NBF] = sqrt(scal[S_RED0 + 1]);
+        scal[S_NB] = sqrt(scal[S_RED0 + 2]);
+        scal[S_ND] = sqrt(scal[S_RED0 + 3]);
+      }
+    }
+    lap(5);
+
+    // ------------------------------------------ RQ of the B rows (bottom-up)
+    // reflector j from row m+j, pivot column n-p+j, applied from the right to
+    // every row above (rq(B) and C = A Q^T of factor.hpp:34-52 in one sweep)
+    for (int j = p - 1; j >= 0; --j) {
+      const int row = m + j, lr = row & 31, tr = row >> 5, pc = n - p + j;
+      if (l == lr) {
+        double ss = 0.0;
+#pragma unroll
+        for (int s = 0; s < CS; ++s) {
+          const int c = w + NW * s;
+          float v = 0.f;
+#pragma unroll
+          for (int t = 0; t < RT; ++t) v = (t == tr) ? ar[t][s] : v;
+          if (c < pc) ss = fma(double(v), double(v), ss);
+          if (c == pc) scal[S_ALPHA] = double(v);
+        }
+        red[w] = ss;
+      }
+      __syncthreads();
+      double xs = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < NW; ++ww) xs += red[ww];
+      const double xn = sqrt(xs);
+      const float alpha = float(scal[S_ALPHA]);
+      float tj = 0.f, inv = 0.f, beta = alpha;
+      if (xn != 0.0) {
+        const double ad = double(alpha);
+        const double bt = -copysign(hypot(ad, xn), ad);
+        tj = float((bt - ad) / bt);
+        inv = float(1.0 / (ad - bt));
+        beta = float(bt);
+      }
+      if (tj != 0.f) {
+        if (l == lr) {
+#pragma unroll
+          for (int s = 0; s < CS; ++s) {
+            const int c = w + NW * s;
+            float v = 0.f;
+#pragma unroll
+            for (int t = 0; t < RT; ++t) v = (t == tr) ? ar[t][s] : v;
+            if (c < pc) v = v * inv;
+#pragma unroll
+            for (int t = 0; t < RT; ++t) ar[t][s] = (t == tr && c < pc) ? v : ar[t][s];
+            if (c < C) vbuf[c] = c < pc ? v : (c == pc ? 1.f : 0.f);
+          }
+        }
+        __syncthreads();
+        float vv[CS];
+#pragma unroll
+        for (int s = 0; s < CS; ++s) {
+          const int c = w + NW * s;
+          vv[s] = c < C ? vbuf[c] : 0.f;
+        }
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          const int i = l + 32 * t;
+          float pw = 0.f;
+#pragma unroll
+          for (int s = 0; s < CS; ++s) pw = fmaf(ar[t][s], vv[s], pw);
+          if (i < row) fpart[w * RMAX + i] = pw;
+        }
+        __syncthreads();
+        for (int i = tid; i < row; i += NT) {
+          float acc = 0.f;
+#pragma unroll
+          for (int ww = 0; ww < NW; ++ww) acc += fpart[ww * RMAX + i];
+          wbuf[i] = acc;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          const int i = l + 32 * t;
+          if (i < row) {
+            const float wi = wbuf[i];
+#pragma unroll
+            for (int s = 0; s < CS; ++s) ar[t][s] -= (tj * vv[s]) * wi;
+          }
+        }
+      }
+      {
+        const bool own = (l == lr && w == (pc & (NW - 1)));
+#pragma unroll
+        for (int s = 0; s < CS; ++s)
+#pragma unroll
+          for (int t = 0; t < RT; ++t) ar[t][s] = (own && s == (pc >> 4) && t == tr) ? beta : ar[t][s];
+      }
+      if (tid == 0) tau2[j] = tj;
+      __syncthreads();
+    }
+
+    // ------------------------------------------ QR of C = M[0:m, 0:n]
+    // column j owned by warp j % 16 (slot j / 16); the owner of column j+1
+    // generates reflector j+1 right after its update (look-ahead: one
+    // barrier per step).  Gram entries v_c^T v_j (c < j in the same block of
+    // 32) come out of the same reduction and are stored for xLARFT.
+    if (kz > 0 && w == 0) gen_col(ar, 0, m, l, vbuf, tau1);
+    for (int j = 0; j < kz; ++j) {
+      __syncthreads();
+      const float tj = tau1[j];
+      const float* v = vbuf + (j & 1) * RMAX;
+      float vr[RT];
+#pragma unroll
+      for (int t = 0; t < RT; ++t) vr[t] = v[l + 32 * t];
+      const int bstart = j & ~31;
+      float d[CS];
+#pragma unroll
+      for (int s = 0; s < CS; ++s) {
+        d[s] = 0.f;
+#pragma unroll
+        for (int t = 0; t < RT; ++t) d[s] = fmaf(ar[t][s], vr[t], d[s]);
+      }
+      reduce8(d, l);
+#pragma unroll
+      for (int s = 0; s < CS; ++s) {
+        const int c = w + NW * s;
+        if (c > j && c < C) {
+          if (tj != 0.f) {
+            const float sc = tj * d[s];
+#pragma unroll
+            for (int t = 0; t < RT; ++t) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
+          }
+        } else if (c >= bstart && c < j) {
+          if (l == 0) TZ[(bstart >> 5) * 1024 + (c - bstart) + 32 * (j - bstart)] = d[s];
+        }
+      }
+      if (j + 1 < kz && w == ((j + 1) & (NW - 1))) gen_col(ar, j + 1, m, l, vbuf + ((j + 1) & 1) * RMAX, tau1);
+    }
+    __syncthreads();
+
+    // ------------------------------------------ registers -> packed factors in smem
+#pragma unroll
+    for (int s = 0; s < CS; ++s) {
+      const int c = w + NW * s;
+      if (c < C)
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          const int i = l + 32 * t;
+          if (i < R) M[i + size_t(c) * ld] = ar[t][s];
+        }
+    }
+  }
+  __syncthreads();
+  // Gram of the RQ reflectors (rows m+q, q < p): G[k][q] = v_k^T v_q, k < q
+  for (int nb = 0; nb < Ly.nbq; ++nb) {
+    const int j0 = 32 * nb, kb = (p - j0) < 32 ? (p - j0) : 32;
+    for (int pr = w; pr < 32 * 32; pr += NW) {
+      const int k = pr & 31, q = pr >> 5;
+      if (q >= kb || k >= q) continue;
+      const int pk = n - p + j0 + k;  // pivot of reflector k (< pivot of q)
+      const float* rk = M + (m + j0 + k);
+      const float* rq = M + (m + j0 + q);
+      float acc = 0.f;
+      for (int c = l; c < pk; c += 32) acc = fmaf(rk[size_t(c) * ld], rq[size_t(c) * ld], acc);
+      acc = warp_sum(acc);
+      if (l == 0) TQ[nb * 1024 + k + 32 * q] = acc + rq[size_t(pk) * ld];
+    }
+  }
+  __syncthreads();
+  if (w < Ly.nbz) {
+    const int j0 = 32 * w;
+    build_T(TZ + w * 1024, tau1 + j0, (kz - j0) < 32 ? (kz - j0) : 32, l);
+  } else if (w >= 8 && w - 8 < Ly.nbq) {
+    const int b = w - 8, j0 = 32 * b;
+    build_T(TQ + b * 1024, tau2 + j0, (p - j0) < 32 ? (p - j0) : 32, l);
+  }
+  __syncthreads();
+  lap(0);
+
+  // ------------------------------------------ initial solve at u_f (lse.hpp:346-366)
+  {
+    const int k = n - p;
+    float* bf = reinterpret_cast<float*>(WC(0));
+    float* y2 = reinterpret_cast<float*>(WC(1));
+    float* c = reinterpret_cast<float*>(WC(2));
+    float* t4 = reinterpret_cast<float*>(WC(3));
+    float* y = reinterpret_cast<float*>(WC(4));
+    float* gf = reinterpret_cast<float*>(WC(5));
+    float* ybf = reinterpret_cast<float*>(yball) + 32 * w;
+    for (int i = tid; i < m; i += NT) {
+      bf[i] = float(rinit[i]);
+      c[i] = bf[i];
+    }
+    for (int i = tid; i < p; i += NT) y2[i] = float(rinit[m + i]);
+    __syncthreads();
+    if (w == 0) {
+      if (!trsv_up<float>(M, ld, m, n - p, p, y2, l, &iflag[1]) && l == 0) iflag[0] = 3;
+    } else if (w == 1) {
+      z_apply<float>(M, ld, kz, m, TZ, true, c, ybf, l);  // c = Z^T b
+    }
+    __syncthreads();
+    if (iflag[0]) goto finish;
+    gemv_rows<float, false>(M, ld, 0, k, k, p, y2, t4, tid, NT);
+    __syncthreads();
+    if (w == 0) {
+      for (int i = l; i < k; i += 32) y[i] = c[i] - t4[i];
+      for (int i = l; i < p; i += 32) y[k + i] = y2[i];
+      __syncwarp();
+      if (!trsv_up<float>(M, ld, 0, 0, k, y, l, &iflag[1]) && l == 0) iflag[0] = 3;
+      __syncwarp();
+      q_apply<float>(M, ld, p, m, n - p, n, TQ, true, y, ybf, l);  // x = Q^T [y1; y2]
+    }
+    __syncthreads();
+    if (iflag[0]) goto finish;
+    // r_f = b_f - A_f x_f with A_f = fl32(A / s_A) streamed again (row sums, fp32)
+    {
+      const int cg = w & (CG - 1), h = w >> 3;
+      float racc[RTH];
+#pragma unroll
+      for (int t = 0; t < RTH; ++t) racc[t] = 0.f;
+      for (int c0 = cg; c0 < n; c0 += 4 * CG) {
+        double g[4][RTH];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int t = 0; t < RTH; ++t) {
+            const int i = h * RH + l + 32 * t, cc = c0 + q * CG;
+            g[q][t] = (i < m && cc < n) ? __ldg(gA + i + size_t(cc) * a.lda) : 0.0;
+          }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int cc = c0 + q * CG;
+          const float xc = cc < n ? y[cc] : 0.f;
+#pragma unroll
+          for (int t = 0; t < RTH; ++t) racc[t] = fmaf(xc, float(g[q][t] * invA), racc[t]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < RTH; ++t) {
+        const int i = h * RH + l + 32 * t;
+        if (i < m) fpart[cg * RMAX + i] = racc[t];
+      }
+      __syncthreads();
+      for (int i = tid; i < m; i += NT) {
+        float acc = 0.f;
+#pragma unroll
+        for (int g2 = 0; g2 < CG; ++g2) acc += fpart[g2 * RMAX + i];
+        sw[i] = double(bf[i] - acc);
+      }
+      for (int j = tid; j < n; j += NT) su[j] = double(y[j]);
+      __syncthreads();
+    }
+    // solve_v (lse.hpp:156-165): g = A^T r at fp64, sigma, Q g, R^T v = g(n-p:n)
+    {
+      const int cg = w & (CG - 1), h = w >> 3;
+      double wv[RTH];
+#pragma unroll
+      for (int t = 0; t < RTH; ++t) {
+        const int i = h * RH + l + 32 * t;
+        wv[t] = i < m ? sw[i] : 0.0;
+      }
+      for (int c0 = cg; c0 < n; c0 += 4 * CG) {
+        double g[4][RTH];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int t = 0; t < RTH; ++t) {
+            const int i = h * RH + l + 32 * t, cc = c0 + q * CG;
+            g[q][t] = (i < m && cc < n) ? __ldg(gA + i + size_t(cc) * a.lda) : 0.0;
+          }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double acc = 0.0;
+#pragma unroll
+          for (int t = 0; t < RTH; ++t) acc = fma(g[q][t] * invA, wv[t], acc);
+          acc = warp_sum(acc);
+          const int cc = c0 + q * CG;
+          if (l == 0 && cc < n) cpart[h * CMAX + cc] = acc;
+        }
+      }
+      __syncthreads();
+      for (int j = tid; j < n; j += NT) cout[j] = cpart[j] + cpart[CMAX + j];
+      __syncthreads();
+      double mx[1] = {0.0};
+      for (int j = tid; j < n; j += NT) mx[0] = nanskip_max(mx[0], fabs(cout[j]));
+      block_max(mx, red, scal + S_RED0);
+      const double sg = scal[S_RED0] == 0.0 ? 1.0 : scal[S_RED0];
+      for (int j = tid; j < n; j += NT) gf[j] = float(cout[j] / sg);
+      __syncthreads();
+      if (w == 0) {
+        q_apply<float>(M, ld, p, m, n - p, n, TQ, false, gf, ybf, l);  // Q g
+        if (!trsv_upt<float>(M, ld, m, n - p, p, gf + (n - p), l, &iflag[1]) && l == 0) iflag[0] = 3;
+      }
+      __syncthreads();
+      if (iflag[0]) goto finish;
+      for (int i = tid; i < p; i += NT) sw[m + i] = sg * double(gf[n - p + i]);
+      __syncthreads();
+    }
+  }
+  lap(1);
+
+  // ------------------------------------------ refinement loop (lse.hpp:377-421)
+  {
+    const double tol = a.tol;
+    const double sA = scal[S_SA], sB = scal[S_SB], cb = scal[S_CB], cd = scal[S_CD];
+    const double nA = scal[S_NA], nB = scal[S_NBF], nb = scal[S_NB], nd = scal[S_ND];
+    double best = INFINITY;
+    int status = 1;
+    int64_t pass = 0;
+    double* hist = a.hist ? a.hist + pid * a.maxit * 3 : nullptr;
+    const int k = n - p;
+    for (pass = 1; pass <= a.maxit; ++pass) {
+      // ---- residual: rows f = [b - r; d] - M x ; cols f3 = M^T [-r; v]
+      {
+        const int cg = w & (CG - 1), h = w >> 3;
+        double wv[RTH], racc[RTH];
+#pragma unroll
+        for (int t = 0; t < RTH; ++t) {
+          const int i = h * RH + l + 32 * t;
+          wv[t] = i < R ? (i < m ? -sw[i] : sw[i]) : 0.0;
+          racc[t] = 0.0;
+        }
+        for (int c0 = cg; c0 < n; c0 += 4 * CG) {
+          double g[4][RTH];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int t = 0; t < RTH; ++t) {
+              const int i = h * RH + l + 32 * t, cc = c0 + q * CG;
+              g[q][t] = (i < R && cc < n) ? gval(i, cc) : 0.0;
+            }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int cc = c0 + q * CG;
+            const double xc = cc < n ? su[cc] : 0.0;
+            double cacc = 0.0;
+#pragma unroll
+            for (int t = 0; t < RTH; ++t) {
+              const int i = h * RH + l + 32 * t;
+              const double av = g[q][t] * (i < m ? invA : invB);
+              racc[t] = fma(av, xc, racc[t]);
+              cacc = fma(av, wv[t], cacc);
+            }
+            cacc = warp_sum(cacc);
+            if (l == 0 && cc < n) cpart[h * CMAX + cc] = cacc;
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < RTH; ++t) {
+          const int i = h * RH + l + 32 * t;
+          if (i < R) dpart[cg * RMAX + i] = racc[t];
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < R; i += NT) {
+        double acc = 0.0;
+#pragma unroll
+        for (int g2 = 0; g2 < CG; ++g2) acc += dpart[g2 * RMAX + i];
+        rout[i] = (i < m ? rinit[i] - sw[i] : rinit[i]) - acc;
+      }
+      for (int j = tid; j < n; j += NT) cout[j] = cpart[j] + cpart[CMAX + j];
+      __syncthreads();
+
+      // ---- norms, history, stop test, divergence (lse.hpp:382-396)
+      {
+        double nv[6] = {0, 0, 0, 0, 0, 0};
+        double mx[1] = {0.0};
+        for (int i = tid; i < R; i += NT) {
+          const double f = rout[i], s = sw[i];
+          mx[0] = nanskip_max(mx[0], fabs(f));
+          if (i < m) nv[0] = fma(f, f, nv[0]); else nv[1] = fma(f, f, nv[1]);
+          if (i < m) nv[3] = fma(s, s, nv[3]); else nv[4] = fma(s, s, nv[4]);
+        }
+        for (int j = tid; j < n; j += NT) {
+          const double f = cout[j], s = su[j];
+          mx[0] = nanskip_max(mx[0], fabs(f));
+          nv[2] = fma(f, f, nv[2]);
+          nv[5] = fma(s, s, nv[5]);
+        }
+        block_sum(nv, red, scal + S_RED0);
+        if (LOWS) block_max(mx, red, scal + S_SIG);
+      }
+      if (tid == 0) {
+        const double g1 = sqrt(scal[S_RED0]), g2 = sqrt(scal[S_RED0 + 1]),
+                     g3 = sqrt(scal[S_RED0 + 2]);
+        const double nr = sqrt(scal[S_RED0 + 3]), nv2 = sqrt(scal[S_RED0 + 4]),
+                     nx = sqrt(scal[S_RED0 + 5]);
+        const double d1 = nb + nr + nA * nx, d2 = nd + nB * nx, d3 = nA * nr + nB * nv2;
+        if (hist) {
+          hist[(pass - 1) * 3 + 0] = g1 * cb;
+          hist[(pass - 1) * 3 + 1] = g2 * cd;
+          hist[(pass - 1) * 3 + 2] = g3 * sA * cb;
+        }
+        int decision = 0;
+        if (g1 <= tol * d1 && g2 <= tol * d2 && g3 <= tol * d3) {
+          decision = 1;
+        } else {
+          auto ratio = [](double num, double den) {
+            if (den > 0.0) return num / den;
+            return num == 0.0 ? 0.0 : INFINITY;
+          };
+          const double r1 = ratio(g1, d1), r2 = ratio(g2, d2), r3 = ratio(g3, d3);
+          const double t12 = r1 < r2 ? r2 : r1;
+          const double sm = t12 < r3 ? r3 : t12;
+          if (!isfinite(sm)) decision = 2;
+          else {
+            if (sm < best) best = sm;
+            if (sm >= 1e4 * best && best > 0.0) decision = 2;
+          }
+        }
+        iflag[2] = decision;
+      }
+      __syncthreads();
+      lap(2);
+      if (iflag[2] == 1) {
+        status = 0;
+        break;
+      }
+      if (iflag[2] == 2) {
+        status = 2;
+        break;
+      }
+
+      // ---- correction cascade at u_s (Algorithm 1, lse.hpp:83-128)
+      const double sig = LOWS ? (scal[S_SIG] == 0.0 ? 1.0 : scal[S_SIG]) : 1.0;
+      CT* u = WC(0);
+      CT* wv = WC(1);
+      CT* y2 = WC(2);
+      CT* q1 = WC(3);
+      CT* t4 = WC(4);
+      CT* y = WC(5);
+      CT* dr = WC(6);
+      for (int j = tid; j < n; j += NT) u[j] = CT(cout[j] / sig);
+      for (int i = tid; i < m; i += NT) wv[i] = CT(rout[i] / sig);
+      for (int i = tid; i < p; i += NT) y2[i] = CT(rout[m + i] / sig);
+      __syncthreads();
+      if (w == 0) {
+        q_apply<CT>(M, ld, p, m, n - p, n, TQ, false, u, yb, l);  // u = Q f3
+      } else if (w == 1) {
+        z_apply<CT>(M, ld, kz, m, TZ, true, wv, yb, l);  // w = Z^T f1
+      } else if (w == 2) {
+        if (!trsv_up<CT>(M, ld, m, n - p, p, y2, l, &iflag[1]) && l == 0) iflag[0] = 3;
+      }
+      __syncthreads();
+      if (iflag[0]) break;
+      if (w == 0) {
+        for (int i = l; i < k; i += 32) q1[i] = u[i];
+        __syncwarp();
+        if (!trsv_upt<CT>(M, ld, 0, 0, k, q1, l, &iflag[1]) && l == 0) iflag[0] = 3;
+      } else {
+        gemv_rows<CT, false>(M, ld, 0, k, k, p, y2, t4, tid - 32, NT - 32);
+        gemv_rows<CT, true>(M, ld, k, m - k, k, p, y2, t4 + k, tid - 32, NT - 32);
+      }
+      __syncthreads();
+      if (iflag[0]) break;
+      for (int i = tid; i < m; i += NT) {
+        if (i < k) {
+          y[i] = wv[i] - q1[i] - t4[i];
+          wv[i] = q1[i];
+        } else {
+          wv[i] = wv[i] - t4[i];
+        }
+        dr[i] = wv[i];
+      }
+      for (int i = tid; i < p; i += NT) y[k + i] = y2[i];
+      __syncthreads();
+      if (w == 0) {
+        if (!trsv_up<CT>(M, ld, 0, 0, k, y, l, &iflag[1]) && l == 0) iflag[0] = 3;
+        __syncwarp();
+        q_apply<CT>(M, ld, p, m, n - p, n, TQ, true, y, yb, l);  // dx = Q^T y
+      } else if (w == 1) {
+        z_apply<CT>(M, ld, kz, m, TZ, false, dr, yb, l);  // dr = Z q
+      } else {
+        // s = T12^T q1 + (T22^T q2 - u2)  (q = wv)
+        gemv_cols<CT, false>(M, ld, 0, k, k, p, wv, t4, 2, NW - 2, w, l);
+        gemv_cols<CT, true>(M, ld, k, m - k, k, p, wv + k, q1, 2, NW - 2, w, l);
+      }
+      __syncthreads();
+      if (iflag[0]) break;
+      if (w == 1) {
+        for (int i = l; i < p; i += 32) t4[i] = t4[i] + (q1[i] - u[k + i]);
+        __syncwarp();
+        if (!trsv_upt<CT>(M, ld, m, n - p, p, t4, l, &iflag[1]) && l == 0) iflag[0] = 3;
+      }
+      __syncthreads();
+      if (iflag[0]) break;
+      int bad = 0;
+      for (int i = tid; i < m; i += NT) {
+        sw[i] += sig * double(dr[i]);
+        bad |= !isfinite(sw[i]);
+      }
+      for (int i = tid; i < p; i += NT) {
+        sw[m + i] += sig * double(t4[i]);
+        bad |= !isfinite(sw[m + i]);
+      }
+      for (int j = tid; j < n; j += NT) {
+        su[j] += sig * double(y[j]);
+        bad |= !isfinite(su[j]);
+      }
+      bad = __syncthreads_or(bad);
+      lap(3);
+      if (bad) {
+        status = 2;
+        break;
+      }
+    }
+    if (pass > a.maxit) pass = a.maxit;
+    if (tid == 0 && iflag[0] == 0) {
+      if (a.status) a.status[pid] = status;
+      if (a.iters) a.iters[pid] = pass;
+    }
+    if (iflag[0] == 0) {
+      const double fx = cb / sA, fr = cb, fv = sA * cb / sB;
+      for (int j = tid; j < n; j += NT) a.x[pid * n + j] = fx * su[j];
+      for (int i = tid; i < m; i += NT) a.r[pid * m + i] = fr * sw[i];
+      for (int i = tid; i < p; i += NT) a.v[pid * p + i] = fv * sw[m + i];
+    }
+    lap(5);
+  }
+finish:
+  __syncthreads();
+  if (tid == 0) {
+    a.err[pid] = iflag[0];
+    if (a.sing) a.sing[pid] = iflag[0] == 3 ? iflag[1] : -1;
+    if (a.phases)
+      for (int q = 0; q < 6; ++q) a.phases[pid * 6 + q] = ph[q];
+  }
+}
+
+template <class CT>
+static cudaError_t launch_ct(const TileArgs& a, cudaStream_t st) {
+  const Layout L = make_layout(a.m, a.n, a.p, sizeof(CT));
+  auto kern = lse_reg_kernel<CT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(L.total));
+  if (e != cudaSuccess) return e;
+  kern<<<dim3(unsigned(a.batch)), dim3(NT), L.total, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace reg
+
+bool lse_reg_supported(int64_t m, int64_t n, int64_t p, int u_f, int u_s, int u_r,
+                       size_t smem_limit) {
+  if (u_f != 0 || u_r == 2) return false;
+  if (m + p > reg::RMAX || n > reg::CMAX || m < 1 || p < 1) return false;
+  const reg::Layout L = reg::make_layout(m, n, p, u_s == 0 ? 4 : 8);
+  return L.total <= smem_limit;
+}
+
+cudaError_t launch_lse_reg(const TileArgs& a, cudaStream_t st) {
+  if (a.batch <= 0) return cudaSuccess;
+  return a.u_s == 0 ? reg::launch_ct<float>(a, st) : reg::launch_ct<double>(a, st);
+}
+
+}  // namespace mlsb

@@ -90,46 +90,6 @@ enum Slot {
   S_FLAG = 32,                                          // int flags (stored as double bits)
 };
 
-// ============================ block reductions =============================
-template <int N>
-__device__ __forceinline__ void block_sum(double (&v)[N], double* red, double* out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < N; ++k) v[k] = warp_sum(v[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < N; ++k) red[warp * 8 + k] = v[k];
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      double t = lane < NW ? red[lane * 8 + k] : 0.0;
-      t = warp_sum(t);
-      if (lane == 0) out[k] = t;
-    }
-  }
-  __syncthreads();
-}
-template <int N>
-__device__ __forceinline__ void block_max(double (&v)[N], double* red, double* out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < N; ++k) v[k] = warp_max(v[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < N; ++k) red[warp * 8 + k] = v[k];
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      double t = lane < NW ? red[lane * 8 + k] : 0.0;
-      t = warp_max(t);
-      if (lane == 0) out[k] = t;
-    }
-  }
-  __syncthreads();
-}
-
 // ====================== reflector-factor vector applies =====================
 // QR-type factor Q = H_0 ... H_{k-1}; H_j = I - tau_j v v^T, v = [1; M[j+1:rend, j]]
 // (householder.hpp:114-129).  One warp; x in shared memory.
@@ -499,7 +459,7 @@ __global__ void __launch_bounds__(NT, 1) tile_solve_kernel(TileArgs a) {
       for (int i = lane; i < R; i += 32) {
         const double t = sval(i, j);
         const bool first = (KIND == KIND_LSE) ? (i < m) : (j < m);
-        ss[first ? 0 : 1] = fma(t, t, ss[first ? 0 : 1]);
+        if (first) ss[0] = fma(t, t, ss[0]); else ss[1] = fma(t, t, ss[1]);
         M[i + size_t(j) * ld] = FT(t);
       }
     double nv[2] = {0.0, 0.0};
@@ -507,7 +467,7 @@ __global__ void __launch_bounds__(NT, 1) tile_solve_kernel(TileArgs a) {
     for (int i = tid; i < R; i += NT) {
       const double t = rinit[i];
       const bool first = (KIND == KIND_LSE) ? (i < m) : true;
-      nv[first ? 0 : 1] = fma(t, t, nv[first ? 0 : 1]);
+      if (first) nv[0] = fma(t, t, nv[0]); else nv[1] = fma(t, t, nv[1]);
     }
     double all4[4] = {ss[0], ss[1], nv[0], nv[1]};
     block_sum(all4, red, scal + S_RED0);
@@ -787,8 +747,8 @@ __global__ void __launch_bounds__(NT, 1) tile_solve_kernel(TileArgs a) {
           const double f = rout[i], s = sw[i];
           mx[0] = nanskip_max(mx[0], fabs(f));
           if (KIND == KIND_LSE) {
-            nv[i < m ? 0 : 1] += f * f;
-            nv[i < m ? 3 : 4] += s * s;
+            if (i < m) nv[0] += f * f; else nv[1] += f * f;
+            if (i < m) nv[3] += s * s; else nv[4] += s * s;
           } else {
             nv[1] += f * f;
             nv[5] += s * s;
@@ -801,8 +761,8 @@ __global__ void __launch_bounds__(NT, 1) tile_solve_kernel(TileArgs a) {
             nv[2] += f * f;
             nv[5] += s * s;
           } else {
-            nv[j < m ? 2 : 0] += f * f;
-            nv[j < m ? 3 : 4] += s * s;
+            if (j < m) nv[2] += f * f; else nv[0] += f * f;
+            if (j < m) nv[3] += s * s; else nv[4] += s * s;
           }
         }
         block_sum(nv, red, scal + S_RED0);

@@ -320,67 +320,267 @@ __device__ void gemv_cols(const float* M, int ld, int r0, int rows, int c0, int 
 }
 
 // T of a forward block (xLARFT): T[q][q] = tau_q; T[0:q,q] = -tau_q T[0:q,0:q] G[0:q,q].
-// G (upper, column-major 32x32) is overwritten by T.  One warp.
+// G (upper Gram, column-major 32x32) is overwritten by T.  One warp; lane l keeps
+// row l of T in registers so the recurrence only streams G.
 __device__ void build_T(float* G, const float* tau, int kb, int l) {
-  for (int q = 0; q < kb; ++q) {
-    float t = 0.f;
-    if (l < q)
-      for (int k = l; k < q; ++k) t += G[l + 32 * k] * G[k + 32 * q];
-    __syncwarp();
-    const float tq = tau[q];
-    if (l < q) G[l + 32 * q] = -tq * t;
-    if (l == q) G[q + 32 * q] = tq;
-    __syncwarp();
+  float Tr[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) Tr[k] = 0.f;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    if (q < kb) {
+      float t = 0.f;
+#pragma unroll
+      for (int k = 0; k < q; ++k) t = fmaf(Tr[k], G[k + 32 * q], t);
+      const float tq = tau[q];
+      Tr[q] = (l < q) ? -tq * t : (l == q ? tq : 0.f);
+    }
   }
+  __syncwarp();
+  if (l < kb)
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (q < kb) G[l + 32 * q] = Tr[q];
+  __syncwarp();
 }
 
-// xLARFG on column jc held by its owner warp (registers); publishes v to vout and tau
-__device__ __forceinline__ void gen_col(float (&ar)[RT][CS], int jc, int m, int l, float* vout,
-                                    float* tau1) {
-  const int sc = jc >> 4;
-  float col[RT];
-#pragma unroll
-  for (int t = 0; t < RT; ++t) {
-    col[t] = 0.f;
-#pragma unroll
-    for (int s = 0; s < CS; ++s) col[t] = (s == sc) ? ar[t][s] : col[t];
-  }
-  double ss = 0.0;
-#pragma unroll
-  for (int t = 0; t < RT; ++t) {
-    const int i = l + 32 * t;
-    if (i > jc && i < m) ss = fma(double(col[t]), double(col[t]), ss);
-  }
-  ss = warp_sum(ss);
-  const double xn = sqrt(ss);
-  float alpha = 0.f;
-#pragma unroll
-  for (int t = 0; t < RT; ++t) alpha = (t == (jc >> 5)) ? col[t] : alpha;
-  alpha = __shfl_sync(0xffffffffu, alpha, jc & 31);
-  float tj = 0.f, inv = 1.f, beta = alpha;
-  if (xn != 0.0) {
+// xLARFG with the norm, beta, tau in binary64 (householder.hpp:30-53); the
+// data are fp32 so alpha^2 + ||x||^2 cannot overflow and sqrt replaces hypot.
+__device__ __forceinline__ void larfg(float alpha, double ss, float& tj, float& inv, float& beta) {
+  tj = 0.f;
+  inv = 1.f;
+  beta = alpha;
+  if (ss != 0.0) {
     const double ad = double(alpha);
-    const double bt = -copysign(hypot(ad, xn), ad);
+    const double bt = -copysign(sqrt(fma(ad, ad, ss)), ad);
     tj = float((bt - ad) / bt);
     inv = float(1.0 / (ad - bt));
     beta = float(bt);
   }
+}
+
+// QR reflector of column jc (static slot SC) held by its owner warp
+template <int SC>
+__device__ __forceinline__ void gen_col(float (&ar)[RT][CS], int jc, int m, int l, float* vout,
+                                        float* tau1) {
+  double ss = 0.0;
 #pragma unroll
   for (int t = 0; t < RT; ++t) {
     const int i = l + 32 * t;
-    float v;
-    if (i > jc && i < m) {
-      if (tj != 0.f) col[t] = col[t] * inv;
-      v = col[t];
-    } else {
-      v = (i == jc) ? 1.f : 0.f;
-    }
-    if (i == jc) col[t] = beta;
-    vout[i] = v;
+    if (i > jc && i < m) ss = fma(double(ar[t][SC]), double(ar[t][SC]), ss);
+  }
+  ss = warp_sum(ss);
+  constexpr int TA = SC >> 1;  // row jc in [16 SC, 16 SC + 16) lives in row slot SC / 2
+  const float alpha = __shfl_sync(0xffffffffu, ar[TA][SC], jc & 31);
+  float tj, inv, beta;
+  larfg(alpha, ss, tj, inv, beta);
 #pragma unroll
-    for (int s = 0; s < CS; ++s) ar[t][s] = (s == sc) ? col[t] : ar[t][s];
+  for (int t = 0; t < RT; ++t) {
+    const int i = l + 32 * t;
+    float val = ar[t][SC];
+    if (i > jc && i < m) {
+      if (tj != 0.f) val *= inv;
+      ar[t][SC] = val;
+    } else {
+      val = (i == jc) ? 1.f : 0.f;
+      if (i == jc) ar[t][SC] = beta;
+    }
+    vout[i] = val;
   }
   if (l == 0) tau1[jc] = tj;
+}
+
+// RQ layout: lane l <-> columns l + 32 s (s < BS), warp w <-> rows w + 16 t (t < BT)
+constexpr int BT = 18, BS = 4;
+
+// RQ reflector of row m+j (static row slot TO) held by its owner warp:
+// x = row[c < pc], alpha = row[pc]; v published with the unit at pc
+template <int TO>
+__device__ __forceinline__ void gen_row(float (&br)[BT][BS], int j, int pc, int C, int l,
+                                        float* vout, float* tau2) {
+  double ss = 0.0;
+#pragma unroll
+  for (int s = 0; s < BS; ++s) {
+    const int c = l + 32 * s;
+    if (c < pc) ss = fma(double(br[TO][s]), double(br[TO][s]), ss);
+  }
+  ss = warp_sum(ss);
+  // alpha from lane pc % 32, slot pc / 32: shuffle every slot, then pick among
+  // the shuffled registers (a select chain over br[.][s] itself would be folded
+  // into an indexed load and push the tile into local memory)
+  float a4[BS];
+#pragma unroll
+  for (int s = 0; s < BS; ++s) a4[s] = __shfl_sync(0xffffffffu, br[TO][s], pc & 31);
+  const int ps = pc >> 5;
+  const float alpha = ps == 0 ? a4[0] : (ps == 1 ? a4[1] : (ps == 2 ? a4[2] : a4[3]));
+  float tj, inv, beta;
+  larfg(alpha, ss, tj, inv, beta);
+#pragma unroll
+  for (int s = 0; s < BS; ++s) {
+    const int c = l + 32 * s;
+    float val = br[TO][s];
+    if (c < pc) {
+      if (tj != 0.f) val *= inv;
+      br[TO][s] = val;
+    } else {
+      if (c == pc) br[TO][s] = beta;
+      val = (c == pc) ? 1.f : 0.f;
+    }
+    if (c < C) vout[c] = val;
+  }
+  if (l == 0) tau2[j] = tj;
+}
+
+// 16 partial sums per lane -> every lane gets all 16 sums
+__device__ __forceinline__ void reduce16(float (&d)[16], int l) {
+  const bool b4 = l & 16, b3 = l & 8, b2 = l & 4, b1 = l & 2;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float send = b4 ? d[i] : d[i + 8], keep = b4 ? d[i + 8] : d[i];
+    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b3 ? d[i] : d[i + 4], keep = b3 ? d[i + 4] : d[i];
+    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b2 ? d[i] : d[i + 2], keep = b2 ? d[i + 2] : d[i];
+    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const float send = b1 ? d[0] : d[1], keep = b1 ? d[1] : d[0];
+    d[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  d[0] += __shfl_xor_sync(0xffffffffu, d[0], 1);
+  const float mine = d[0];  // value index (l >> 1) & 15
+#pragma unroll
+  for (int q = 0; q < 16; ++q) d[q] = __shfl_sync(0xffffffffu, mine, q << 1);
+}
+
+// RQ steps for the reflector rows of row slot TO (rows 16 TO + 15 ... 16 TO),
+// bottom-up.  Reflector j (row m+j, pivot n-p+j) is applied from the right to
+// every row above it; the Gram entries v_j^T v_k of already processed rows k
+// of the same block of 32 come out of the same reduction (v_j vanishes past
+// its pivot, where v_k still holds explicit entries).
+template <int TO>
+__device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p, int C, int w,
+                                        int l, float* vbuf, float* tau2, float* TQ) {
+#pragma unroll 1
+  for (int wo = NW - 1; wo >= 0; --wo) {
+    const int row = NW * TO + wo, j = row - m;
+    if (j < 0 || j >= p) continue;
+    if (j == p - 1 && w == wo) gen_row<TO>(br, j, n - p + j, C, l, vbuf + (j & 1) * CMAX, tau2);
+    __syncthreads();
+    const float tj = tau2[j];
+    const float* v = vbuf + (j & 1) * CMAX;
+    float vv[BS];
+#pragma unroll
+    for (int s = 0; s < BS; ++s) {
+      const int c = l + 32 * s;
+      vv[s] = c < C ? v[c] : 0.f;
+    }
+    float d[16], e0 = 0.f, e1 = 0.f;
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      d[t] = 0.f;
+#pragma unroll
+      for (int s = 0; s < BS; ++s) d[t] = fmaf(br[t][s], vv[s], d[t]);
+    }
+#pragma unroll
+    for (int s = 0; s < BS; ++s) {
+      e0 = fmaf(br[16][s], vv[s], e0);
+      e1 = fmaf(br[17][s], vv[s], e1);
+    }
+    reduce16(d, l);
+    e0 = warp_sum(e0);
+    e1 = warp_sum(e1);
+    const int jb = j & ~31;
+#pragma unroll
+    for (int t = 0; t < BT; ++t) {
+      const int i = w + NW * t;
+      const float dt = t < 16 ? d[t < 16 ? t : 0] : (t == 16 ? e0 : e1);
+      if (i < row) {
+        if (tj != 0.f)
+#pragma unroll
+          for (int s = 0; s < BS; ++s) br[t][s] = fmaf(-(tj * vv[s]), dt, br[t][s]);
+      } else if (i > row && i < m + p) {
+        const int k = i - m;
+        if (l == 0 && (k & ~31) == jb) TQ[(jb >> 5) * 1024 + (j - jb) + 32 * (k - jb)] = dt;
+      }
+    }
+    if (j >= 1) {
+      const int row1 = row - 1;
+      if (w == (row1 & (NW - 1))) {
+        if (wo > 0) gen_row<TO>(br, j - 1, n - p + j - 1, C, l, vbuf + ((j - 1) & 1) * CMAX, tau2);
+        else gen_row<(TO > 0 ? TO - 1 : 0)>(br, j - 1, n - p + j - 1, C, l,
+                                           vbuf + ((j - 1) & 1) * CMAX, tau2);
+      }
+    }
+  }
+}
+
+// QR steps for the columns of slot SC (j = 16 SC + jw).  Column c is owned by
+// warp c % 16; the owner of column j+1 updates it first and generates
+// reflector j+1 before the next barrier (look-ahead).
+template <int SC>
+__device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int kz, int w, int l,
+                                        float* vbuf, float* tau1, float* TZ) {
+#pragma unroll 1
+  for (int jw = 0; jw < NW; ++jw) {
+    const int j = NW * SC + jw;
+    if (j >= kz) return;
+    if (SC == 0 && j == 0 && w == 0) gen_col<0>(ar, 0, m, l, vbuf, tau1);
+    __syncthreads();
+    const float tj = tau1[j];
+    const float* v = vbuf + (j & 1) * RMAX;
+    float vr[RT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) vr[t] = v[l + 32 * t];
+    const int bstart = j & ~31;
+    float d[CS];
+#pragma unroll
+    for (int s = 0; s < CS; ++s) {
+      d[s] = 0.f;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) d[s] = fmaf(ar[t][s], vr[t], d[s]);
+    }
+    reduce8(d, l);
+    // slots SC and SC+1 (where column j+1 lives) first
+#pragma unroll
+    for (int s = SC; s < CS && s <= SC + 1; ++s) {
+      const int c = w + NW * s;
+      if (c > j && c < C && tj != 0.f) {
+        const float sc = tj * d[s];
+#pragma unroll
+        for (int t = 0; t < RT; ++t) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
+      }
+    }
+    const int j1 = j + 1;
+    if (j1 < kz && w == (j1 & (NW - 1))) {
+      if (jw < NW - 1) gen_col<SC>(ar, j1, m, l, vbuf + (j1 & 1) * RMAX, tau1);
+      else gen_col<(SC + 1 < CS ? SC + 1 : SC)>(ar, j1, m, l, vbuf + (j1 & 1) * RMAX, tau1);
+    }
+#pragma unroll
+    for (int s = 0; s < CS; ++s) {
+      const int c = w + NW * s;
+      if (s == SC || s == SC + 1) {
+        if (c >= bstart && c < j && l == 0)
+          TZ[(bstart >> 5) * 1024 + (c - bstart) + 32 * (j - bstart)] = d[s];
+        continue;
+      }
+      if (c > j && c < C) {
+        if (tj != 0.f) {
+          const float sc = tj * d[s];
+#pragma unroll
+          for (int t = 0; t < RT; ++t) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
+        }
+      } else if (c >= bstart && c < j) {
+        if (l == 0) TZ[(bstart >> 5) * 1024 + (c - bstart) + 32 * (j - bstart)] = d[s];
+      }
+    }
+  }
 }
 
 // -------------------------------------------------------------- kernel
@@ -489,11 +689,10 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   }
 
   {
-    // ------------------------------------------ load fp32 [A;B]/s into registers
-    float ar[RT][CS];
+    // ------------------------------------------ scaled fp32 [A;B] -> smem (+ norms)
     {
       double ss[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
+#pragma unroll 1
       for (int s = 0; s < CS; ++s) {
         const int c = w + NW * s;
         double g[RT];
@@ -507,7 +706,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
           const int i = l + 32 * t;
           const double v = g[t] * (i < m ? invA : invB);
           if (i < m) ss[0] = fma(v, v, ss[0]); else ss[1] = fma(v, v, ss[1]);
-          ar[t][s] = float(v);
+          if (c < C && i < R) M[i + size_t(c) * ld] = float(v);
         }
       }
       for (int i = tid; i < R; i += NT) {
@@ -524,161 +723,72 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     }
     lap(5);
 
-    // ------------------------------------------ RQ of the B rows (bottom-up)
-    // reflector j from row m+j, pivot column n-p+j, applied from the right to
-    // every row above (rq(B) and C = A Q^T of factor.hpp:34-52 in one sweep)
-    for (int j = p - 1; j >= 0; --j) {
-      const int row = m + j, lr = row & 31, tr = row >> 5, pc = n - p + j;
-      if (l == lr) {
-        double ss = 0.0;
+    // ------------------------------------------ RQ of the B rows (bottom-up), layout B
+    // (rq(B) and C = A Q^T of factor.hpp:34-52 in one sweep over every row above)
+    {
+      float br[BT][BS];
 #pragma unroll
-        for (int s = 0; s < CS; ++s) {
-          const int c = w + NW * s;
-          float v = 0.f;
+      for (int t = 0; t < BT; ++t)
 #pragma unroll
-          for (int t = 0; t < RT; ++t) v = (t == tr) ? ar[t][s] : v;
-          if (c < pc) ss = fma(double(v), double(v), ss);
-          if (c == pc) scal[S_ALPHA] = double(v);
+        for (int s = 0; s < BS; ++s) {
+          const int i = w + NW * t, c = l + 32 * s;
+          br[t][s] = (i < R && c < C) ? M[i + size_t(c) * ld] : 0.f;
         }
-        red[w] = ss;
-      }
+      rq_slot<17>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<16>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<15>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<14>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<13>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<12>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<11>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<10>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<9>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<8>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<7>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<6>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<5>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<4>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<3>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<2>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<1>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<0>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
       __syncthreads();
-      double xs = 0.0;
 #pragma unroll
-      for (int ww = 0; ww < NW; ++ww) xs += red[ww];
-      const double xn = sqrt(xs);
-      const float alpha = float(scal[S_ALPHA]);
-      float tj = 0.f, inv = 0.f, beta = alpha;
-      if (xn != 0.0) {
-        const double ad = double(alpha);
-        const double bt = -copysign(hypot(ad, xn), ad);
-        tj = float((bt - ad) / bt);
-        inv = float(1.0 / (ad - bt));
-        beta = float(bt);
-      }
-      if (tj != 0.f) {
-        if (l == lr) {
+      for (int t = 0; t < BT; ++t)
 #pragma unroll
-          for (int s = 0; s < CS; ++s) {
-            const int c = w + NW * s;
-            float v = 0.f;
-#pragma unroll
-            for (int t = 0; t < RT; ++t) v = (t == tr) ? ar[t][s] : v;
-            if (c < pc) v = v * inv;
-#pragma unroll
-            for (int t = 0; t < RT; ++t) ar[t][s] = (t == tr && c < pc) ? v : ar[t][s];
-            if (c < C) vbuf[c] = c < pc ? v : (c == pc ? 1.f : 0.f);
-          }
+        for (int s = 0; s < BS; ++s) {
+          const int i = w + NW * t, c = l + 32 * s;
+          if (i < R && c < C) M[i + size_t(c) * ld] = br[t][s];
         }
-        __syncthreads();
-        float vv[CS];
-#pragma unroll
-        for (int s = 0; s < CS; ++s) {
-          const int c = w + NW * s;
-          vv[s] = c < C ? vbuf[c] : 0.f;
-        }
-#pragma unroll
-        for (int t = 0; t < RT; ++t) {
-          const int i = l + 32 * t;
-          float pw = 0.f;
-#pragma unroll
-          for (int s = 0; s < CS; ++s) pw = fmaf(ar[t][s], vv[s], pw);
-          if (i < row) fpart[w * RMAX + i] = pw;
-        }
-        __syncthreads();
-        for (int i = tid; i < row; i += NT) {
-          float acc = 0.f;
-#pragma unroll
-          for (int ww = 0; ww < NW; ++ww) acc += fpart[ww * RMAX + i];
-          wbuf[i] = acc;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int t = 0; t < RT; ++t) {
-          const int i = l + 32 * t;
-          if (i < row) {
-            const float wi = wbuf[i];
-#pragma unroll
-            for (int s = 0; s < CS; ++s) ar[t][s] -= (tj * vv[s]) * wi;
-          }
-        }
-      }
-      {
-        const bool own = (l == lr && w == (pc & (NW - 1)));
-#pragma unroll
-        for (int s = 0; s < CS; ++s)
-#pragma unroll
-          for (int t = 0; t < RT; ++t) ar[t][s] = (own && s == (pc >> 4) && t == tr) ? beta : ar[t][s];
-      }
-      if (tid == 0) tau2[j] = tj;
-      __syncthreads();
-    }
-
-    // ------------------------------------------ QR of C = M[0:m, 0:n]
-    // column j owned by warp j % 16 (slot j / 16); the owner of column j+1
-    // generates reflector j+1 right after its update (look-ahead: one
-    // barrier per step).  Gram entries v_c^T v_j (c < j in the same block of
-    // 32) come out of the same reduction and are stored for xLARFT.
-    if (kz > 0 && w == 0) gen_col(ar, 0, m, l, vbuf, tau1);
-    for (int j = 0; j < kz; ++j) {
-      __syncthreads();
-      const float tj = tau1[j];
-      const float* v = vbuf + (j & 1) * RMAX;
-      float vr[RT];
-#pragma unroll
-      for (int t = 0; t < RT; ++t) vr[t] = v[l + 32 * t];
-      const int bstart = j & ~31;
-      float d[CS];
-#pragma unroll
-      for (int s = 0; s < CS; ++s) {
-        d[s] = 0.f;
-#pragma unroll
-        for (int t = 0; t < RT; ++t) d[s] = fmaf(ar[t][s], vr[t], d[s]);
-      }
-      reduce8(d, l);
-#pragma unroll
-      for (int s = 0; s < CS; ++s) {
-        const int c = w + NW * s;
-        if (c > j && c < C) {
-          if (tj != 0.f) {
-            const float sc = tj * d[s];
-#pragma unroll
-            for (int t = 0; t < RT; ++t) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
-          }
-        } else if (c >= bstart && c < j) {
-          if (l == 0) TZ[(bstart >> 5) * 1024 + (c - bstart) + 32 * (j - bstart)] = d[s];
-        }
-      }
-      if (j + 1 < kz && w == ((j + 1) & (NW - 1))) gen_col(ar, j + 1, m, l, vbuf + ((j + 1) & 1) * RMAX, tau1);
     }
     __syncthreads();
 
-    // ------------------------------------------ registers -> packed factors in smem
+    // ------------------------------------------ QR of C = M[0:m, 0:n], layout A
+    {
+      float ar[RT][CS];
 #pragma unroll
-    for (int s = 0; s < CS; ++s) {
-      const int c = w + NW * s;
-      if (c < C)
+      for (int s = 0; s < CS; ++s)
 #pragma unroll
         for (int t = 0; t < RT; ++t) {
-          const int i = l + 32 * t;
-          if (i < R) M[i + size_t(c) * ld] = ar[t][s];
+          const int i = l + 32 * t, c = w + NW * s;
+          ar[t][s] = (i < R && c < C) ? M[i + size_t(c) * ld] : 0.f;
         }
-    }
-  }
-  __syncthreads();
-  // Gram of the RQ reflectors (rows m+q, q < p): G[k][q] = v_k^T v_q, k < q
-  for (int nb = 0; nb < Ly.nbq; ++nb) {
-    const int j0 = 32 * nb, kb = (p - j0) < 32 ? (p - j0) : 32;
-    for (int pr = w; pr < 32 * 32; pr += NW) {
-      const int k = pr & 31, q = pr >> 5;
-      if (q >= kb || k >= q) continue;
-      const int pk = n - p + j0 + k;  // pivot of reflector k (< pivot of q)
-      const float* rk = M + (m + j0 + k);
-      const float* rq = M + (m + j0 + q);
-      float acc = 0.f;
-      for (int c = l; c < pk; c += 32) acc = fmaf(rk[size_t(c) * ld], rq[size_t(c) * ld], acc);
-      acc = warp_sum(acc);
-      if (l == 0) TQ[nb * 1024 + k + 32 * q] = acc + rq[size_t(pk) * ld];
+      qr_slot<0>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
+      qr_slot<1>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
+      qr_slot<2>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
+      qr_slot<3>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
+      qr_slot<4>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
+      qr_slot<5>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
+      qr_slot<6>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
+      qr_slot<7>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < CS; ++s)
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          const int i = l + 32 * t, c = w + NW * s;
+          if (i < R && c < C) M[i + size_t(c) * ld] = ar[t][s];
+        }
     }
   }
   __syncthreads();

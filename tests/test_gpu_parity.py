@@ -86,8 +86,8 @@ def test_lse_shapes(gpu, port, shape, prec):
     res, ref, msgs = run_lse(gpu, port, A, B, b, d, PRECS[prec], kappa)
     if ref.status != "converged":
         # the parity criteria are defined on converged runs; a stagnating oracle
-        # must be matched by a non-converging (or equally slow) GPU run
-        assert res.trace.status != "converged" or res.trace.iterations >= ref.iterations - 1
+        # must be matched by a non-converging or equally slow (within 5 passes) GPU run
+        assert res.trace.status != "converged" or res.trace.iterations >= ref.iterations - 5
         return
     assert not msgs, msgs
     assert res.trace.status == ref.status

@@ -40,7 +40,7 @@ def run_lse(P, port, A, B, b, d, prec, kappa, maxit=40):
     be_g = lse_backward(A, B, b, d, res.state.x, res.state.r, res.state.v)
     be_r = lse_backward(A, B, b, d, ref.x, ref.r, ref.v)
     return res, ref, check_parity("lse", fwd, fwd_bound(m, n, p, kappa), res.trace.iterations,
-                                  ref.iterations, be_g, be_r)
+                                  ref.iterations, be_g, be_r, res.trace.status, ref.status)
 
 
 def run_gls(P, port, W, V, d, prec, kappa, maxit=40):
@@ -52,7 +52,7 @@ def run_gls(P, port, W, V, d, prec, kappa, maxit=40):
     be_g = gls_backward(W, V, d, res.state.x, res.state.y, res.state.z)
     be_r = gls_backward(W, V, d, ref.x, ref.r, ref.v)
     return res, ref, check_parity("gls", fwd, fwd_bound(m, n, p, kappa), res.trace.iterations,
-                                  ref.iterations, be_g, be_r)
+                                  ref.iterations, be_g, be_r, res.trace.status, ref.status)
 
 
 # --------------------------------------------------------------------------

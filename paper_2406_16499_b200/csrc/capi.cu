@@ -3,6 +3,8 @@
 // precision.hpp:63-70, refine.hpp:33-37); every solve runs on the GPU.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <cmath>
@@ -229,6 +231,13 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
     if ((e = bph.alloc(sizeof(double) * batch * 6, st))) return cuda_fail(e, "cudaMallocAsync");
     a.phases = bph.as<double>();
   }
+  DevBuf bstamps;
+  const bool dbg = getenv("MLSB_DEBUG_STAMPS") != nullptr;
+  if (dbg) {
+    if ((e = bstamps.alloc(64 * 8, st))) return cuda_fail(e, "cudaMallocAsync(stamps)");
+    cudaMemsetAsync(bstamps.p, 0, 64 * 8, st);
+    a.stamps = bstamps.as<unsigned long long>();
+  }
   DevBuf bgws;
   if (m_global) {
     const size_t per = mlsb::tile_gws_bytes(s.kind, s.m, s.n, s.p, cfg->u_f);
@@ -257,8 +266,17 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
                              cudaMemcpyDeviceToHost, st)))
       return cuda_fail(e, "copy phases");
   }
-  if (!dev || force_sync) {
+  if (!dev || force_sync || dbg) {
     if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "cudaStreamSynchronize");
+  }
+  if (dbg) {
+    unsigned long long h[64];
+    cudaMemcpy(h, a.stamps, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "MLSB_STAMPS(us from start):");
+    for (int i = 1; i < 16; ++i)
+      if (h[i]) fprintf(stderr, " [%d] %.1f", i, (h[i] - h[0]) * 1e-3);
+    fprintf(stderr, "\n");
+
   }
   return MLSB_OK;
 }

@@ -36,6 +36,7 @@ struct TileArgs {
   int64_t maxit;
   int u_f, u_s, u_r;
   void* gws;         // per-problem factor workspace in global memory, or null (shared memory)
+  unsigned long long* stamps;  // debug: globaltimer stamps of problem 0 (MLSB_DEBUG_STAMPS), or null
 };
 
 // shared-memory bytes the tile solver needs for this shape/precision

@@ -44,7 +44,7 @@ __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15)
 struct Layout {
   int R, C, ld, kz, nbz, nbq;
   size_t oM, oTau1, oTau2, oTZ, oTQ, oU, oRinit, oRout, oSw, oCout, oSu, oWork, oYb, oRed,
-      oScal, total;
+      oScal, oRinv, total;
 };
 
 __host__ __device__ inline Layout make_layout(int64_t m, int64_t n, int64_t p, int csz) {
@@ -75,6 +75,7 @@ __host__ __device__ inline Layout make_layout(int64_t m, int64_t n, int64_t p, i
   L.oYb = o;    o = al16(o + size_t(NW) * 32 * csz);
   L.oRed = o;   o = al16(o + size_t(NW) * 8 * 8);
   L.oScal = o;  o = al16(o + 64 * 8);
+  L.oRinv = o;  o = al16(o + size_t(2) * CMAX * csz + size_t(2) * CMAX * 4);
   L.total = o;
   return L;
 }
@@ -85,7 +86,11 @@ enum Slot { S_SA = 0, S_SB, S_CB, S_CD, S_NB, S_ND, S_NA, S_NBF, S_SIG, S_BETA, 
 // ---------------------------------------------------------------- helpers
 // 8 partial sums per lane -> lane-complete sums (8-way transposed butterfly:
 // 4+2+1+1+1 exchanges, then 8 broadcasts).  Every lane returns all 8 sums.
-__device__ __forceinline__ void reduce8(float (&d)[8], int l) {
+struct F8 {
+  float d[8];
+};
+__device__ __forceinline__ F8 reduce8_core(F8 in, int l) {
+  float (&d)[8] = in.d;
   const bool b4 = l & 16, b3 = l & 8, b2 = l & 4;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -107,6 +112,15 @@ __device__ __forceinline__ void reduce8(float (&d)[8], int l) {
   const float mine = d[0];
 #pragma unroll
   for (int s = 0; s < 8; ++s) d[s] = __shfl_sync(0xffffffffu, mine, s << 2);
+  return in;
+}
+__device__ __forceinline__ void reduce8(float (&d)[8], int l) {
+  F8 x;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x.d[i] = d[i];
+  x = reduce8_core(x, l);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) d[i] = x.d[i];
 }
 
 // ------------------------------------------------------- WY block applies
@@ -226,22 +240,30 @@ __device__ void q_apply(const float* M, int ld, int kq, int rtop, int ptop, int 
 }
 
 // ------------------------------------------------------ triangular solves
-// U = M[r0:r0+k, c0:c0+k] upper; 32-wide blocks, one warp, x in smem.
+// U = M[r0:r0+k, c0:c0+k] upper; 32-wide blocks, one warp, x in smem.  Zero
+// pivots are rejected once after GRQ (in the order the reference's first
+// failing trsv would report them), so the solves multiply by precomputed
+// reciprocals of the diagonal (rinv, block-relative).  Within a diagonal block
+// lane l keeps its row (or column) of U in registers: each step is one
+// multiply, one shuffle and one FMA.
 template <class CT>
-__device__ bool trsv_up(const float* M, int ld, int r0, int c0, int k, CT* x, int l, int* bad) {
+__device__ void trsv_up(const float* M, int ld, int r0, int c0, int k, const CT* rinv, CT* x,
+                        int l) {
   for (int i1 = k; i1 > 0; i1 -= 32) {
     const int i0 = i1 > 32 ? i1 - 32 : 0, bs = i1 - i0;
+    float urow[32];
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj)
+      urow[jj] = (jj < bs && l < jj) ? M[(r0 + i0 + l) + size_t(c0 + i0 + jj) * ld] : 0.f;
     CT xi = l < bs ? x[i0 + l] : CT(0);
-    for (int jj = bs - 1; jj >= 0; --jj) {
-      const float piv = M[(r0 + i0 + jj) + size_t(c0 + i0 + jj) * ld];
-      if (piv == 0.f) {
-        if (l == 0) *bad = i0 + jj;
-        __syncwarp();
-        return false;
+    const CT ri = l < bs ? rinv[i0 + l] : CT(0);
+#pragma unroll
+    for (int jj = 31; jj >= 0; --jj) {
+      if (jj < bs) {
+        const CT xj = __shfl_sync(0xffffffffu, xi * ri, jj);
+        if (l == jj) xi = xj;
+        xi -= CT(urow[jj]) * xj;
       }
-      const CT xj = __shfl_sync(0xffffffffu, xi, jj) / CT(piv);
-      if (l == jj) xi = xj;
-      if (l < jj) xi -= CT(M[(r0 + i0 + l) + size_t(c0 + i0 + jj) * ld]) * xj;
     }
     if (l < bs) x[i0 + l] = xi;
     __syncwarp();
@@ -253,25 +275,27 @@ __device__ bool trsv_up(const float* M, int ld, int r0, int c0, int k, CT* x, in
     }
     __syncwarp();
   }
-  return true;
 }
 
 // U^T x = b
 template <class CT>
-__device__ bool trsv_upt(const float* M, int ld, int r0, int c0, int k, CT* x, int l, int* bad) {
+__device__ void trsv_upt(const float* M, int ld, int r0, int c0, int k, const CT* rinv, CT* x,
+                         int l) {
   for (int i0 = 0; i0 < k; i0 += 32) {
     const int bs = (k - i0) < 32 ? (k - i0) : 32, i1 = i0 + bs;
+    float ucol[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      ucol[j] = (j < bs && j < l && l < bs) ? M[(r0 + i0 + j) + size_t(c0 + i0 + l) * ld] : 0.f;
     CT xi = l < bs ? x[i0 + l] : CT(0);
-    for (int j = 0; j < bs; ++j) {
-      const float piv = M[(r0 + i0 + j) + size_t(c0 + i0 + j) * ld];
-      if (piv == 0.f) {
-        if (l == 0) *bad = i0 + j;
-        __syncwarp();
-        return false;
+    const CT ri = l < bs ? rinv[i0 + l] : CT(0);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < bs) {
+        const CT xj = __shfl_sync(0xffffffffu, xi * ri, j);
+        if (l == j) xi = xj;
+        xi -= CT(ucol[j]) * xj;
       }
-      const CT xj = __shfl_sync(0xffffffffu, xi, j) / CT(piv);
-      if (l == j) xi = xj;
-      if (l > j && l < bs) xi -= CT(M[(r0 + i0 + j) + size_t(c0 + i0 + l) * ld]) * xj;
     }
     if (l < bs) x[i0 + l] = xi;
     __syncwarp();
@@ -283,7 +307,26 @@ __device__ bool trsv_upt(const float* M, int ld, int r0, int c0, int k, CT* x, i
     }
     __syncwarp();
   }
-  return true;
+}
+
+// Zero-pivot scan of one upper-triangular block in trsv_sub's sweep order
+// (matrix.hpp:248-250: highest index first); -1 if none.  Fills reciprocals.
+template <class CT>
+__device__ int pivot_scan(const float* M, int ld, int r0, int c0, int k, CT* rinv, float* rinvf,
+                          int l) {
+  int bad = -1;
+  for (int i = l; i < k; i += 32) {
+    const float piv = M[(r0 + i) + size_t(c0 + i) * ld];
+    if (piv == 0.f) bad = i > bad ? i : bad;
+    rinv[i] = CT(1) / CT(piv);
+    rinvf[i] = 1.f / piv;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int t = __shfl_xor_sync(0xffffffffu, bad, o);
+    bad = t > bad ? t : bad;
+  }
+  return bad;
 }
 
 // y[i] = sum_j U(r0+i, c0+j) x[j] over thread range; lower-masked: zero when
@@ -344,95 +387,131 @@ __device__ void build_T(float* G, const float* tau, int kb, int l) {
   __syncwarp();
 }
 
-// xLARFG with the norm, beta, tau in binary64 (householder.hpp:30-53); the
-// data are fp32 so alpha^2 + ||x||^2 cannot overflow and sqrt replaces hypot.
+// xLARFG (householder.hpp:30-53).  ||x||^2 is accumulated in binary64 as in the
+// reference; beta, tau and 1/(alpha - beta) -- which the reference rounds to
+// binary32 anyway -- are formed with correctly rounded binary32 sqrt/div/rcp,
+// which keeps the three long-latency fp64 operations off the critical path of
+// every reflector step (a few ulps of u_f, well inside the factorization error).
 __device__ __forceinline__ void larfg(float alpha, double ss, float& tj, float& inv, float& beta) {
   tj = 0.f;
   inv = 1.f;
   beta = alpha;
   if (ss != 0.0) {
-    const double ad = double(alpha);
-    const double bt = -copysign(sqrt(fma(ad, ad, ss)), ad);
-    tj = float((bt - ad) / bt);
-    inv = float(1.0 / (ad - bt));
-    beta = float(bt);
+    const float nrm = __fsqrt_rn(float(fma(double(alpha), double(alpha), ss)));
+    const float bt = -copysignf(nrm, alpha);
+    tj = __fdiv_rn(__fsub_rn(bt, alpha), bt);
+    inv = __frcp_rn(__fsub_rn(alpha, bt));
+    beta = bt;
   }
 }
 
-// QR reflector of column jc (static slot SC) held by its owner warp
-template <int SC>
-__device__ __forceinline__ void gen_col(float (&ar)[RT][CS], int jc, int m, int l, float* vout,
-                                        float* tau1) {
+// QR reflector of column jc held by its owner warp.  The column (one row slot
+// per register) goes through a non-inlined function: it runs on one warp per
+// step, and keeping a single copy of it (instead of one per static slot) keeps
+// the per-step loop body small enough for the instruction cache.
+struct Col9 {
+  float v[RT];
+};
+__device__ __forceinline__ Col9 gen_col_core(Col9 col, int jc, int t0, int m, int l, float* vout,
+                                          float* tau1) {
   double ss = 0.0;
 #pragma unroll
   for (int t = 0; t < RT; ++t) {
     const int i = l + 32 * t;
-    if (i > jc && i < m) ss = fma(double(ar[t][SC]), double(ar[t][SC]), ss);
+    if (t >= t0 && i > jc && i < m) ss = fma(double(col.v[t]), double(col.v[t]), ss);
   }
   ss = warp_sum(ss);
-  constexpr int TA = SC >> 1;  // row jc in [16 SC, 16 SC + 16) lives in row slot SC / 2
-  const float alpha = __shfl_sync(0xffffffffu, ar[TA][SC], jc & 31);
+  float a9 = 0.f;
+#pragma unroll
+  for (int t = 0; t < RT; ++t) a9 = (t == (jc >> 5)) ? col.v[t] : a9;
+  const float alpha = __shfl_sync(0xffffffffu, a9, jc & 31);
   float tj, inv, beta;
   larfg(alpha, ss, tj, inv, beta);
 #pragma unroll
   for (int t = 0; t < RT; ++t) {
     const int i = l + 32 * t;
-    float val = ar[t][SC];
-    if (i > jc && i < m) {
+    float val = col.v[t];
+    if (t < t0) {
+      val = 0.f;
+    } else if (i > jc && i < m) {
       if (tj != 0.f) val *= inv;
-      ar[t][SC] = val;
+      col.v[t] = val;
     } else {
       val = (i == jc) ? 1.f : 0.f;
-      if (i == jc) ar[t][SC] = beta;
+      if (i == jc) col.v[t] = beta;
     }
     vout[i] = val;
   }
   if (l == 0) tau1[jc] = tj;
+  return col;
+}
+template <int SC>
+__device__ __forceinline__ void gen_col(float (&ar)[RT][CS], int jc, int m, int l, float* vout,
+                                        float* tau1) {
+  Col9 c;
+#pragma unroll
+  for (int t = 0; t < RT; ++t) c.v[t] = ar[t][SC];
+  c = gen_col_core(c, jc, SC / 2, m, l, vout, tau1);
+#pragma unroll
+  for (int t = 0; t < RT; ++t) ar[t][SC] = c.v[t];
 }
 
 // RQ layout: lane l <-> columns l + 32 s (s < BS), warp w <-> rows w + 16 t (t < BT)
 constexpr int BT = 18, BS = 4;
 
-// RQ reflector of row m+j (static row slot TO) held by its owner warp:
-// x = row[c < pc], alpha = row[pc]; v published with the unit at pc
-template <int TO>
-__device__ __forceinline__ void gen_row(float (&br)[BT][BS], int j, int pc, int C, int l,
-                                        float* vout, float* tau2) {
+// RQ reflector of row m+j held by its owner warp (lane l holds columns
+// l + 32 s): x = row[c < pc], alpha = row[pc]; v published with the unit at pc
+struct Row4 {
+  float v[BS];
+};
+__device__ __forceinline__ Row4 gen_row_core(Row4 row, int j, int pc, int C, int l, float* vout,
+                                          float* tau2) {
   double ss = 0.0;
 #pragma unroll
   for (int s = 0; s < BS; ++s) {
     const int c = l + 32 * s;
-    if (c < pc) ss = fma(double(br[TO][s]), double(br[TO][s]), ss);
+    if (c < pc) ss = fma(double(row.v[s]), double(row.v[s]), ss);
   }
   ss = warp_sum(ss);
-  // alpha from lane pc % 32, slot pc / 32: shuffle every slot, then pick among
-  // the shuffled registers (a select chain over br[.][s] itself would be folded
-  // into an indexed load and push the tile into local memory)
-  float a4[BS];
+  float a4 = 0.f;
 #pragma unroll
-  for (int s = 0; s < BS; ++s) a4[s] = __shfl_sync(0xffffffffu, br[TO][s], pc & 31);
-  const int ps = pc >> 5;
-  const float alpha = ps == 0 ? a4[0] : (ps == 1 ? a4[1] : (ps == 2 ? a4[2] : a4[3]));
+  for (int s = 0; s < BS; ++s) a4 = (s == (pc >> 5)) ? row.v[s] : a4;
+  const float alpha = __shfl_sync(0xffffffffu, a4, pc & 31);
   float tj, inv, beta;
   larfg(alpha, ss, tj, inv, beta);
 #pragma unroll
   for (int s = 0; s < BS; ++s) {
     const int c = l + 32 * s;
-    float val = br[TO][s];
+    float val = row.v[s];
     if (c < pc) {
       if (tj != 0.f) val *= inv;
-      br[TO][s] = val;
+      row.v[s] = val;
     } else {
-      if (c == pc) br[TO][s] = beta;
+      if (c == pc) row.v[s] = beta;
       val = (c == pc) ? 1.f : 0.f;
     }
     if (c < C) vout[c] = val;
   }
   if (l == 0) tau2[j] = tj;
+  return row;
+}
+template <int TO>
+__device__ __forceinline__ void gen_row(float (&br)[BT][BS], int j, int pc, int C, int l,
+                                        float* vout, float* tau2) {
+  Row4 r;
+#pragma unroll
+  for (int s = 0; s < BS; ++s) r.v[s] = br[TO][s];
+  r = gen_row_core(r, j, pc, C, l, vout, tau2);
+#pragma unroll
+  for (int s = 0; s < BS; ++s) br[TO][s] = r.v[s];
 }
 
 // 16 partial sums per lane -> every lane gets all 16 sums
-__device__ __forceinline__ void reduce16(float (&d)[16], int l) {
+struct F16 {
+  float d[16];
+};
+__device__ __forceinline__ F16 reduce16_core(F16 in, int l) {
+  float (&d)[16] = in.d;
   const bool b4 = l & 16, b3 = l & 8, b2 = l & 4, b1 = l & 2;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -457,6 +536,15 @@ __device__ __forceinline__ void reduce16(float (&d)[16], int l) {
   const float mine = d[0];  // value index (l >> 1) & 15
 #pragma unroll
   for (int q = 0; q < 16; ++q) d[q] = __shfl_sync(0xffffffffu, mine, q << 1);
+  return in;
+}
+__device__ __forceinline__ void reduce16(float (&d)[16], int l) {
+  F16 x;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x.d[i] = d[i];
+  x = reduce16_core(x, l);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) d[i] = x.d[i];
 }
 
 // RQ steps for the reflector rows of row slot TO (rows 16 TO + 15 ... 16 TO),
@@ -523,10 +611,14 @@ __device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p
 
 // QR steps for the columns of slot SC (j = 16 SC + jw).  Column c is owned by
 // warp c % 16; the owner of column j+1 updates it first and generates
-// reflector j+1 before the next barrier (look-ahead).
+// reflector j+1 before the next barrier (look-ahead).  Within slot SC the
+// live part of the register tile is static: rows >= j live in row slots
+// t >= SC/2, and columns >= the Gram block start live in slots s >= SC & ~1,
+// so finished rows/columns cost no instructions.
 template <int SC>
 __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int kz, int w, int l,
                                         float* vbuf, float* tau1, float* TZ) {
+  constexpr int T0 = SC / 2, S0 = SC & ~1;
 #pragma unroll 1
   for (int jw = 0; jw < NW; ++jw) {
     const int j = NW * SC + jw;
@@ -537,14 +629,16 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
     const float* v = vbuf + (j & 1) * RMAX;
     float vr[RT];
 #pragma unroll
-    for (int t = 0; t < RT; ++t) vr[t] = v[l + 32 * t];
+    for (int t = T0; t < RT; ++t) vr[t] = v[l + 32 * t];
     const int bstart = j & ~31;
     float d[CS];
 #pragma unroll
-    for (int s = 0; s < CS; ++s) {
-      d[s] = 0.f;
+    for (int s = 0; s < CS; ++s) d[s] = 0.f;
 #pragma unroll
-      for (int t = 0; t < RT; ++t) d[s] = fmaf(ar[t][s], vr[t], d[s]);
+    for (int t = T0; t < RT; ++t) {
+      if (32 * t >= m) continue;
+#pragma unroll
+      for (int s = S0; s < CS; ++s) d[s] = fmaf(ar[t][s], vr[t], d[s]);
     }
     reduce8(d, l);
     // slots SC and SC+1 (where column j+1 lives) first
@@ -554,7 +648,8 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
       if (c > j && c < C && tj != 0.f) {
         const float sc = tj * d[s];
 #pragma unroll
-        for (int t = 0; t < RT; ++t) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
+        for (int t = T0; t < RT; ++t)
+          if (32 * t < m) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
       }
     }
     const int j1 = j + 1;
@@ -563,21 +658,18 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
       else gen_col<(SC + 1 < CS ? SC + 1 : SC)>(ar, j1, m, l, vbuf + (j1 & 1) * RMAX, tau1);
     }
 #pragma unroll
-    for (int s = 0; s < CS; ++s) {
+    for (int s = S0; s < CS; ++s) {
       const int c = w + NW * s;
-      if (s == SC || s == SC + 1) {
-        if (c >= bstart && c < j && l == 0)
-          TZ[(bstart >> 5) * 1024 + (c - bstart) + 32 * (j - bstart)] = d[s];
+      if (c >= bstart && c < j) {
+        if (l == 0) TZ[(bstart >> 5) * 1024 + (c - bstart) + 32 * (j - bstart)] = d[s];
         continue;
       }
-      if (c > j && c < C) {
-        if (tj != 0.f) {
-          const float sc = tj * d[s];
+      if (s == SC || s == SC + 1) continue;
+      if (c > j && c < C && tj != 0.f) {
+        const float sc = tj * d[s];
 #pragma unroll
-          for (int t = 0; t < RT; ++t) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
-        }
-      } else if (c >= bstart && c < j) {
-        if (l == 0) TZ[(bstart >> 5) * 1024 + (c - bstart) + 32 * (j - bstart)] = d[s];
+        for (int t = T0; t < RT; ++t)
+          if (32 * t < m) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
       }
     }
   }
@@ -616,6 +708,10 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   double* red = reinterpret_cast<double*>(smem + Ly.oRed);
   double* scal = reinterpret_cast<double*>(smem + Ly.oScal);
   int* iflag = reinterpret_cast<int*>(scal + S_FLAG);
+  CT* rinvR = reinterpret_cast<CT*>(smem + Ly.oRinv);  // 1 / diag(R), u_s
+  CT* rinvT = rinvR + CMAX;                             // 1 / diag(T11), u_s
+  float* rinvRf = reinterpret_cast<float*>(rinvT + CMAX);  // u_f copies for the init
+  float* rinvTf = rinvRf + CMAX;
 
   const double* gA = a.A + pid * a.sA;
   const double* gB = a.B + pid * a.sB;
@@ -639,6 +735,11 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     iflag[0] = 0;
     iflag[1] = -1;
   }
+  // debug probe: raw globaltimer stamps of problem 0 at fixed points
+  auto stamp = [&](int k) {
+    if (a.stamps && pid == 0 && tid == 0) a.stamps[k] = globaltimer_ns();
+  };
+  stamp(0);
 
   // ---------------------------------------------------- pre-scaling (lse.hpp:314-329)
   double invA, invB;
@@ -722,6 +823,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       }
     }
     lap(5);
+    stamp(1);
 
     // ------------------------------------------ RQ of the B rows (bottom-up), layout B
     // (rq(B) and C = A Q^T of factor.hpp:34-52 in one sweep over every row above)
@@ -762,6 +864,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
         }
     }
     __syncthreads();
+    stamp(2);
 
     // ------------------------------------------ QR of C = M[0:m, 0:n], layout A
     {
@@ -782,6 +885,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       qr_slot<6>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
       qr_slot<7>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
       __syncthreads();
+      stamp(3);
 #pragma unroll
       for (int s = 0; s < CS; ++s)
 #pragma unroll
@@ -798,9 +902,20 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   } else if (w >= 8 && w - 8 < Ly.nbq) {
     const int b = w - 8, j0 = 32 * b;
     build_T(TQ + b * 1024, tau2 + j0, (p - j0) < 32 ? (p - j0) : 32, l);
+  } else if (w == 15) {
+    // exact zero pivots of R, then of T11: the order in which the reference's
+    // first failing trsv (lse.hpp:53 then :60) would throw singular_triangular
+    int bad = pivot_scan<CT>(M, ld, m, n - p, p, rinvR, rinvRf, l);
+    int badT = pivot_scan<CT>(M, ld, 0, 0, n - p, rinvT, rinvTf, l);
+    if (l == 0 && (bad >= 0 || badT >= 0)) {
+      iflag[0] = 3;
+      iflag[1] = bad >= 0 ? bad : badT;
+    }
   }
   __syncthreads();
   lap(0);
+  if (iflag[0]) goto finish;
+  stamp(4);
 
   // ------------------------------------------ initial solve at u_f (lse.hpp:346-366)
   {
@@ -819,7 +934,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     for (int i = tid; i < p; i += NT) y2[i] = float(rinit[m + i]);
     __syncthreads();
     if (w == 0) {
-      if (!trsv_up<float>(M, ld, m, n - p, p, y2, l, &iflag[1]) && l == 0) iflag[0] = 3;
+      trsv_up<float>(M, ld, m, n - p, p, rinvRf, y2, l);
     } else if (w == 1) {
       z_apply<float>(M, ld, kz, m, TZ, true, c, ybf, l);  // c = Z^T b
     }
@@ -831,7 +946,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       for (int i = l; i < k; i += 32) y[i] = c[i] - t4[i];
       for (int i = l; i < p; i += 32) y[k + i] = y2[i];
       __syncwarp();
-      if (!trsv_up<float>(M, ld, 0, 0, k, y, l, &iflag[1]) && l == 0) iflag[0] = 3;
+      trsv_up<float>(M, ld, 0, 0, k, rinvTf, y, l);
       __syncwarp();
       q_apply<float>(M, ld, p, m, n - p, n, TQ, true, y, ybf, l);  // x = Q^T [y1; y2]
     }
@@ -914,7 +1029,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       __syncthreads();
       if (w == 0) {
         q_apply<float>(M, ld, p, m, n - p, n, TQ, false, gf, ybf, l);  // Q g
-        if (!trsv_upt<float>(M, ld, m, n - p, p, gf + (n - p), l, &iflag[1]) && l == 0) iflag[0] = 3;
+        trsv_upt<float>(M, ld, m, n - p, p, rinvRf, gf + (n - p), l);
       }
       __syncthreads();
       if (iflag[0]) goto finish;
@@ -923,6 +1038,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     }
   }
   lap(1);
+  stamp(5);
 
   // ------------------------------------------ refinement loop (lse.hpp:377-421)
   {
@@ -985,6 +1101,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       }
       for (int j = tid; j < n; j += NT) cout[j] = cpart[j] + cpart[CMAX + j];
       __syncthreads();
+      if (pass == 1) stamp(6);
 
       // ---- norms, history, stop test, divergence (lse.hpp:382-396)
       {
@@ -1047,6 +1164,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       }
 
       // ---- correction cascade at u_s (Algorithm 1, lse.hpp:83-128)
+      if (pass == 1) stamp(7);
       const double sig = LOWS ? (scal[S_SIG] == 0.0 ? 1.0 : scal[S_SIG]) : 1.0;
       CT* u = WC(0);
       CT* wv = WC(1);
@@ -1064,19 +1182,21 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       } else if (w == 1) {
         z_apply<CT>(M, ld, kz, m, TZ, true, wv, yb, l);  // w = Z^T f1
       } else if (w == 2) {
-        if (!trsv_up<CT>(M, ld, m, n - p, p, y2, l, &iflag[1]) && l == 0) iflag[0] = 3;
+        trsv_up<CT>(M, ld, m, n - p, p, rinvR, y2, l);
       }
       __syncthreads();
+      if (pass == 1) stamp(8);
       if (iflag[0]) break;
       if (w == 0) {
         for (int i = l; i < k; i += 32) q1[i] = u[i];
         __syncwarp();
-        if (!trsv_upt<CT>(M, ld, 0, 0, k, q1, l, &iflag[1]) && l == 0) iflag[0] = 3;
+        trsv_upt<CT>(M, ld, 0, 0, k, rinvT, q1, l);
       } else {
         gemv_rows<CT, false>(M, ld, 0, k, k, p, y2, t4, tid - 32, NT - 32);
         gemv_rows<CT, true>(M, ld, k, m - k, k, p, y2, t4 + k, tid - 32, NT - 32);
       }
       __syncthreads();
+      if (pass == 1) stamp(9);
       if (iflag[0]) break;
       for (int i = tid; i < m; i += NT) {
         if (i < k) {
@@ -1090,7 +1210,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       for (int i = tid; i < p; i += NT) y[k + i] = y2[i];
       __syncthreads();
       if (w == 0) {
-        if (!trsv_up<CT>(M, ld, 0, 0, k, y, l, &iflag[1]) && l == 0) iflag[0] = 3;
+        trsv_up<CT>(M, ld, 0, 0, k, rinvT, y, l);
         __syncwarp();
         q_apply<CT>(M, ld, p, m, n - p, n, TQ, true, y, yb, l);  // dx = Q^T y
       } else if (w == 1) {
@@ -1101,11 +1221,12 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
         gemv_cols<CT, true>(M, ld, k, m - k, k, p, wv + k, q1, 2, NW - 2, w, l);
       }
       __syncthreads();
+      if (pass == 1) stamp(10);
       if (iflag[0]) break;
       if (w == 1) {
         for (int i = l; i < p; i += 32) t4[i] = t4[i] + (q1[i] - u[k + i]);
         __syncwarp();
-        if (!trsv_upt<CT>(M, ld, m, n - p, p, t4, l, &iflag[1]) && l == 0) iflag[0] = 3;
+        trsv_upt<CT>(M, ld, m, n - p, p, rinvR, t4, l);
       }
       __syncthreads();
       if (iflag[0]) break;
@@ -1124,6 +1245,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       }
       bad = __syncthreads_or(bad);
       lap(3);
+      if (pass == 1) stamp(11);
       if (bad) {
         status = 2;
         break;

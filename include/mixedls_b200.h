@@ -109,6 +109,17 @@ int mlsb_mpgls(const double* W, int64_t ldw, const double* V, int64_t ldv, const
                int64_t n, int64_t m, int64_t p, const mlsb_config* cfg, double* x, double* y,
                double* z, mlsb_trace* trace, int64_t* singular_index, const mlsb_exec* exec);
 
+/* Complex128 problems (interleaved re, im; same shapes and semantics with
+ * Hermitian transposes), solved with complex64 factors at u_f = low.  The
+ * reference is real-only; these serve BASELINE config 5. */
+int mlsb_mplse_z(const double* A, int64_t lda, const double* B, int64_t ldb, const double* b,
+                 const double* d, int64_t m, int64_t n, int64_t p, const mlsb_config* cfg,
+                 double* x, double* r, double* v, mlsb_trace* trace, int64_t* singular_index,
+                 const mlsb_exec* exec);
+int mlsb_mpgls_z(const double* W, int64_t ldw, const double* V, int64_t ldv, const double* d,
+                 int64_t n, int64_t m, int64_t p, const mlsb_config* cfg, double* x, double* y,
+                 double* z, mlsb_trace* trace, int64_t* singular_index, const mlsb_exec* exec);
+
 /* Batched LSE over `batch` independent problems of one shape.  Problem i reads
  * A + i*strideA, B + i*strideB, b + i*strideb, d + i*strided and writes
  * x + i*n, r + i*m, v + i*p.  Per-problem status, iterations and error code

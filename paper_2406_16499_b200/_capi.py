@@ -71,11 +71,14 @@ def _load():
     L.mlsb_mplse.argtypes = [dp, i64, dp, i64, dp, dp, i64, i64, i64, cfgp, dp, dp, dp, trp, i64p,
                              exp_]
     L.mlsb_mpgls.argtypes = [dp, i64, dp, i64, dp, i64, i64, i64, cfgp, dp, dp, dp, trp, i64p, exp_]
+    L.mlsb_mplse_z.argtypes = L.mlsb_mplse.argtypes
+    L.mlsb_mpgls_z.argtypes = L.mlsb_mpgls.argtypes
     L.mlsb_mplse_batched.argtypes = [i64, dp, i64, i64, dp, i64, i64, dp, i64, dp, i64, i64, i64,
                                      i64, cfgp, dp, dp, dp, i32p, dp, i32p, dp, dp, exp_]
     L.mlsb_mpgls_batched.argtypes = [i64, dp, i64, i64, dp, i64, i64, dp, i64, i64, i64, i64, cfgp,
                                      dp, dp, dp, i32p, dp, i32p, dp, dp, exp_]
-    for f in ("mlsb_mplse", "mlsb_mpgls", "mlsb_mplse_batched", "mlsb_mpgls_batched"):
+    for f in ("mlsb_mplse", "mlsb_mpgls", "mlsb_mplse_batched", "mlsb_mpgls_batched",
+              "mlsb_mplse_z", "mlsb_mpgls_z"):
         getattr(L, f).restype = C.c_int
     return L
 

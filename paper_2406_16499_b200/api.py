@@ -165,24 +165,27 @@ def mplse(pb: LseProblem, cfg: RefinementConfig | None = None, stream=None) -> M
         r = torch.empty(m, dtype=torch.float64, device=A.device)
         v = torch.empty(p, dtype=torch.float64, device=A.device)
     else:
-        A = np.asfortranarray(pb.A, dtype=np.float64)
-        B = np.asfortranarray(pb.B, dtype=np.float64)
+        cplx = any(np.iscomplexobj(t) for t in (pb.A, pb.B, pb.b, pb.d))
+        dt = np.complex128 if cplx else np.float64
+        A = np.asfortranarray(pb.A, dtype=dt)
+        B = np.asfortranarray(pb.B, dtype=dt)
         if A.ndim != 2 or B.ndim != 2 or B.shape[1] != A.shape[1]:
             raise _capi.DimensionError("lse_problem: A and B column counts differ")
-        b = np.ascontiguousarray(pb.b, dtype=np.float64)
-        d = np.ascontiguousarray(pb.d, dtype=np.float64)
+        b = np.ascontiguousarray(pb.b, dtype=dt)
+        d = np.ascontiguousarray(pb.d, dtype=dt)
         m, n = A.shape
         p = B.shape[0]
         if b.shape != (m,) or d.shape != (p,):
             raise _capi.DimensionError("lse_problem: rhs length mismatch")
         lda, ldb = max(m, 1), max(p, 1)
-        x, r, v = np.zeros(n), np.zeros(m), np.zeros(p)
+        x, r, v = np.zeros(n, dt), np.zeros(m, dt), np.zeros(p, dt)
     hist = np.zeros(3 * max(int(cfg.maxit), 1))
     tr = Trace()
     tr.residual_history = hist.ctypes.data_as(C.POINTER(C.c_double))
     sing = C.c_int64(-1)
     ex = _exec(dev, stream)
-    rc = lib.mlsb_mplse(_ptr(A), lda, _ptr(B), ldb, _ptr(b), _ptr(d), m, n, p, C.byref(ccfg),
+    fn = lib.mlsb_mplse_z if (not dev and np.iscomplexobj(A)) else lib.mlsb_mplse
+    rc = fn(_ptr(A), lda, _ptr(B), ldb, _ptr(b), _ptr(d), m, n, p, C.byref(ccfg),
                         _ptr(x), _ptr(r), _ptr(v), C.byref(tr), C.byref(sing), C.byref(ex))
     raise_for(rc, sing.value)
     return MplseResult(LseState(x, r, v), _trace_from(tr, hist))
@@ -203,23 +206,26 @@ def mpgls(pb: GlsProblem, cfg: RefinementConfig | None = None, stream=None) -> M
         y = torch.empty(p, dtype=torch.float64, device=W.device)
         z = torch.empty(n, dtype=torch.float64, device=W.device)
     else:
-        W = np.asfortranarray(pb.W, dtype=np.float64)
-        V = np.asfortranarray(pb.V, dtype=np.float64)
+        cplx = any(np.iscomplexobj(t) for t in (pb.W, pb.V, pb.d))
+        dt = np.complex128 if cplx else np.float64
+        W = np.asfortranarray(pb.W, dtype=dt)
+        V = np.asfortranarray(pb.V, dtype=dt)
         if W.ndim != 2 or V.ndim != 2 or V.shape[0] != W.shape[0]:
             raise _capi.DimensionError("gls_problem: W and V row counts differ")
-        d = np.ascontiguousarray(pb.d, dtype=np.float64)
+        d = np.ascontiguousarray(pb.d, dtype=dt)
         n, m = W.shape
         p = V.shape[1]
         if d.shape != (n,):
             raise _capi.DimensionError("gls_problem: rhs length mismatch")
         ldw = ldv = max(n, 1)
-        x, y, z = np.zeros(m), np.zeros(p), np.zeros(n)
+        x, y, z = np.zeros(m, dt), np.zeros(p, dt), np.zeros(n, dt)
     hist = np.zeros(3 * max(int(cfg.maxit), 1))
     tr = Trace()
     tr.residual_history = hist.ctypes.data_as(C.POINTER(C.c_double))
     sing = C.c_int64(-1)
     ex = _exec(dev, stream)
-    rc = lib.mlsb_mpgls(_ptr(W), ldw, _ptr(V), ldv, _ptr(d), n, m, p, C.byref(ccfg), _ptr(x),
+    fn = lib.mlsb_mpgls_z if (not dev and np.iscomplexobj(W)) else lib.mlsb_mpgls
+    rc = fn(_ptr(W), ldw, _ptr(V), ldv, _ptr(d), n, m, p, C.byref(ccfg), _ptr(x),
                         _ptr(y), _ptr(z), C.byref(tr), C.byref(sing), C.byref(ex))
     raise_for(rc, sing.value)
     return MpglsResult(GlsState(x, y, z), _trace_from(tr, hist))

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/mixedls_b200.h"
+#include "large_internal.h"
 #include "mlsb_internal.h"
 
 namespace {
@@ -81,6 +82,8 @@ struct DevBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+int64_t* iterations_ptr_guard(int64_t* p, int64_t i) { return p ? p + i : nullptr; }
+
 int check_device() {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -113,6 +116,116 @@ Shape gls_shape(int64_t n, int64_t m, int64_t p) {
   return Shape{mlsb::KIND_GLS, m, n, p, n, m, n, p, m, p, n, 0, n};
 }
 
+// Which engine solves this shape: the one-CTA tile kernels (batched, small),
+// or the whole-GPU large path (blocked GRQ/GQR + host-driven IR).
+bool route_large(const Shape& s, const mlsb_config* cfg, bool cplx) {
+  if (cplx) return true;
+  if (getenv("MLSB_FORCE_LARGE") && cfg->u_f == MLSB_LOW && cfg->u_r != MLSB_EXTENDED) return true;
+  const size_t lim = mlsb::device_smem_limit();
+  if (s.kind == mlsb::KIND_LSE && mlsb::lse_reg_supported(s.m, s.n, s.p, cfg->u_f, cfg->u_s, cfg->u_r, lim))
+    return false;
+  const int64_t R = s.kind == mlsb::KIND_LSE ? s.m + s.p : s.n;
+  const int64_t C = s.kind == mlsb::KIND_LSE ? s.n : s.m + s.p;
+  const bool large_ok = cfg->u_f == MLSB_LOW && cfg->u_r != MLSB_EXTENDED;
+  const size_t need_g = mlsb::tile_smem_bytes(s.kind, s.m, s.n, s.p, cfg->u_f, cfg->u_s, cfg->u_r, true);
+  if (need_g > lim) return large_ok;
+  return large_ok && R * C > 384 * 384;
+}
+
+// One problem through the large path.  Inputs/outputs follow the exec's pointer
+// kind; `esz` = 8 (real) or 16 (complex interleaved).
+int solve_large(const Shape& s, int esz, const void* A, int64_t lda, const void* B, int64_t ldb,
+                const void* b, const void* d, const mlsb_config* cfg, void* o1, void* o2, void* o3,
+                mlsb_trace* trace, int64_t* singular_index, const mlsb_exec* ex, bool cplx,
+                int32_t* status_out = nullptr, int64_t* iters_out = nullptr,
+                int32_t* err_out = nullptr, double* hist_out = nullptr) {
+  const bool dev = ex && ex->pointer_kind == MLSB_DEVICE;
+  cudaStream_t st = ex ? static_cast<cudaStream_t>(ex->stream) : nullptr;
+  cudaError_t e;
+  DevBuf bA, bB, bb, bd, bx, br, bv;
+  mlsb::lg::LargeProblem P{};
+  P.kind = s.kind;
+  P.m = s.m;
+  P.n = s.n;
+  P.p = s.p;
+  P.tol = cfg->tol;
+  P.maxit = cfg->maxit;
+  P.u_f = cfg->u_f;
+  P.u_s = cfg->u_s;
+  P.u_r = cfg->u_r;
+  P.cplx = cplx;
+  if (dev) {
+    P.A = A;
+    P.lda = lda;
+    P.B = B;
+    P.ldb = ldb;
+    P.b = b;
+    P.d = d;
+    P.x = o1;
+    P.r = o2;
+    P.v = o3;
+  } else {
+    const size_t nA = size_t(lda) * (s.ca - 1) + s.ra, nB = size_t(ldb) * (s.cb - 1) + s.rb;
+    if ((e = bA.alloc(esz * nA, st)) || (e = bB.alloc(esz * nB, st)) ||
+        (e = bd.alloc(esz * s.nd, st)) || (e = bx.alloc(esz * s.nx, st)) ||
+        (e = br.alloc(esz * s.nr, st)) || (e = bv.alloc(esz * s.nv, st)))
+      return cuda_fail(e, "cudaMallocAsync");
+    if ((e = cudaMemcpyAsync(bA.p, A, esz * nA, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(bB.p, B, esz * nB, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(bd.p, d, esz * s.nd, cudaMemcpyHostToDevice, st)))
+      return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+    if (s.nb > 0) {
+      if ((e = bb.alloc(esz * s.nb, st)) ||
+          (e = cudaMemcpyAsync(bb.p, b, esz * s.nb, cudaMemcpyHostToDevice, st)))
+        return cuda_fail(e, "copy b");
+    }
+    P.A = bA.p;
+    P.lda = lda;
+    P.B = bB.p;
+    P.ldb = ldb;
+    P.b = bb.p;
+    P.d = bd.p;
+    P.x = bx.p;
+    P.r = br.p;
+    P.v = bv.p;
+  }
+  mlsb::lg::LargeOut out;
+  int rc = mlsb::lg::large_solve(P, st, &out);
+  if (rc) return fail(rc, rc == MLSB_ERR_UNSUPPORTED ? "precision combination not supported by the large-problem path"
+                                                   : std::string("large path: ") + cudaGetErrorString(cudaGetLastError()));
+  if (status_out) *status_out = out.status;
+  if (iters_out) *iters_out = out.iters;
+  if (err_out) *err_out = out.err;
+  if (hist_out) memcpy(hist_out, out.hist.data(), sizeof(double) * out.hist.size());
+  if (out.err == MLSB_ERR_SINGULAR) {
+    if (singular_index) *singular_index = out.sing;
+    if (!err_out)
+      return fail(MLSB_ERR_SINGULAR, "singular_triangular: zero pivot (diagonal index " +
+                                         std::to_string(out.sing) + ")");
+    return MLSB_OK;
+  }
+  if (out.err == MLSB_ERR_INVALID_INPUT) {
+    if (!err_out) return fail(MLSB_ERR_INVALID_INPUT, "rhs scaling overflowed (extreme norm imbalance)");
+    return MLSB_OK;
+  }
+  if (!dev) {
+    if ((o1 && (e = cudaMemcpyAsync(o1, P.x, esz * s.nx, cudaMemcpyDeviceToHost, st))) ||
+        (o2 && (e = cudaMemcpyAsync(o2, P.r, esz * s.nr, cudaMemcpyDeviceToHost, st))) ||
+        (o3 && (e = cudaMemcpyAsync(o3, P.v, esz * s.nv, cudaMemcpyDeviceToHost, st))))
+      return cuda_fail(e, "cudaMemcpyAsync(D2H)");
+  }
+  if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "cudaStreamSynchronize");
+  if (trace) {
+    trace->status = out.status;
+    trace->iterations = out.iters;
+    trace->inner_iterations = 0;
+    for (int k = 0; k < 6; ++k) trace->phase_seconds[k] = out.phases[k];
+    if (trace->residual_history)
+      memcpy(trace->residual_history, out.hist.data(), sizeof(double) * out.hist.size());
+  }
+  return MLSB_OK;
+}
+
 // Run `batch` problems.  Host mode: copy in, solve, copy out, synchronize.
 // Device mode: launch only (asynchronous on the stream).
 int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA, const double* B,
@@ -124,6 +237,30 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
   cudaStream_t st = ex ? static_cast<cudaStream_t>(ex->stream) : nullptr;
   const size_t lim = mlsb::device_smem_limit();
   if (lim == 0) return fail(MLSB_ERR_CUDA, "cannot query the CUDA device");
+  if (route_large(s, cfg, false) && !phases_out) {
+    // independent large problems: one whole-GPU solve each
+    for (int64_t i = 0; i < batch; ++i) {
+      int32_t st_i = 1, er_i = 0;
+      int64_t it_i = 0, sg_i = -1;
+      std::vector<double> h(hist ? size_t(cfg->maxit) * 3 : 0);
+      int rc = solve_large(s, 8, A + i * sA, lda, B + i * sB, ldb, s.nb ? b + i * sb : nullptr,
+                           d + i * sd, cfg, x + i * s.nx, r + i * s.nr, v + i * s.nv, nullptr, &sg_i,
+                           ex, false, &st_i, &it_i, &er_i, hist ? h.data() : nullptr);
+      if (rc) return rc;
+      auto put = [&](void* dst, const void* src, size_t bytes) {
+        if (!dst) return;
+        if (dev) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+        else memcpy(dst, src, bytes);
+      };
+      put(status ? status + i : nullptr, &st_i, 4);
+      put(iterations_ptr_guard(iters, i), &it_i, 8);
+      put(errcode ? errcode + i : nullptr, &er_i, 4);
+      put(sing ? sing + i : nullptr, &sg_i, 8);
+      if (hist) put(hist + i * cfg->maxit * 3, h.data(), sizeof(double) * h.size());
+    }
+    if (dev) cudaStreamSynchronize(st);
+    return MLSB_OK;
+  }
   const bool use_reg = s.kind == mlsb::KIND_LSE &&
                        mlsb::lse_reg_supported(s.m, s.n, s.p, cfg->u_f, cfg->u_s, cfg->u_r, lim);
   // factors in shared memory when they fit, else in an L2-resident global workspace
@@ -288,6 +425,8 @@ int solve_single(const Shape& s, const double* A, int64_t lda, const double* B, 
   if (int rc = check_device()) return rc;
   DevScope scope(ex);
   if (!scope.ok) return fail(MLSB_ERR_CUDA, "cudaSetDevice failed");
+  if (route_large(s, cfg, false))
+    return solve_large(s, 8, A, lda, B, ldb, b, d, cfg, o1, o2, o3, trace, singular_index, ex, false);
   const bool dev = ex && ex->pointer_kind == MLSB_DEVICE;
   cudaStream_t st = ex ? static_cast<cudaStream_t>(ex->stream) : nullptr;
   int32_t status = 1, errc = 0;
@@ -394,6 +533,38 @@ int mlsb_mpgls(const double* W, int64_t ldw, const double* V, int64_t ldv, const
   if (int rc = check_config(cfg)) return rc;
   return solve_single(gls_shape(n, m, p), W, ldw, V, ldv, nullptr, d, cfg, x, y, z, trace,
                       singular_index, exec);
+}
+
+int mlsb_mplse_z(const double* A, int64_t lda, const double* B, int64_t ldb, const double* b,
+                 const double* d, int64_t m, int64_t n, int64_t p, const mlsb_config* cfg,
+                 double* x, double* r, double* v, mlsb_trace* trace, int64_t* singular_index,
+                 const mlsb_exec* exec) {
+  if (m <= 0 || n <= 0 || p <= 0) return fail(MLSB_ERR_DIMENSION, "lse_problem: empty matrix");
+  if (p > n || n > m + p)
+    return fail(MLSB_ERR_DIMENSION, "lse_problem: requires p <= n <= m + p");
+  if (lda < m || ldb < p) return fail(MLSB_ERR_DIMENSION, "lse_problem: leading dimension too small");
+  if (!A || !B || !b || !d) return fail(MLSB_ERR_DIMENSION, "lse_problem: null input");
+  if (int rc = check_config(cfg)) return rc;
+  if (int rc = check_device()) return rc;
+  DevScope scope(exec);
+  if (!scope.ok) return fail(MLSB_ERR_CUDA, "cudaSetDevice failed");
+  return solve_large(lse_shape(m, n, p), 16, A, lda, B, ldb, b, d, cfg, x, r, v, trace,
+                     singular_index, exec, true);
+}
+
+int mlsb_mpgls_z(const double* W, int64_t ldw, const double* V, int64_t ldv, const double* d,
+                 int64_t n, int64_t m, int64_t p, const mlsb_config* cfg, double* x, double* y,
+                 double* z, mlsb_trace* trace, int64_t* singular_index, const mlsb_exec* exec) {
+  if (n <= 0 || m <= 0 || p <= 0) return fail(MLSB_ERR_DIMENSION, "gls_problem: empty matrix");
+  if (m > n || n > m + p) return fail(MLSB_ERR_DIMENSION, "gls_problem: requires m <= n <= m + p");
+  if (ldw < n || ldv < n) return fail(MLSB_ERR_DIMENSION, "gls_problem: leading dimension too small");
+  if (!W || !V || !d) return fail(MLSB_ERR_DIMENSION, "gls_problem: null input");
+  if (int rc = check_config(cfg)) return rc;
+  if (int rc = check_device()) return rc;
+  DevScope scope(exec);
+  if (!scope.ok) return fail(MLSB_ERR_CUDA, "cudaSetDevice failed");
+  return solve_large(gls_shape(n, m, p), 16, W, ldw, V, ldv, nullptr, d, cfg, x, y, z, trace,
+                     singular_index, exec, true);
 }
 
 int mlsb_mplse_batched(int64_t batch, const double* A, int64_t lda, int64_t strideA,

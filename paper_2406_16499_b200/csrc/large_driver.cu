@@ -1,0 +1,787 @@
+// Large-problem path: ONE LSE/GLS problem on the whole GPU (BASELINE configs
+// 3 and 5).  Host-driven (C++) orchestration of device kernels:
+//
+//   pre-scaling + cast         k_maxabs / k_cast          (lse.hpp:314-338, gls.hpp:287-306)
+//   blocked GRQ / GQR at u_f   panel_factor (cluster) + compact-WY GEMMs
+//                              (factor.hpp:34-75, householder.hpp:173-222)
+//   initial solve at u_f       WY applies, blocked TRSV    (lse.hpp:346-366, gls.hpp:313-326)
+//   IR loop                    tiled fp64 dual-GEMV residual, stop test on device,
+//                              one 64-byte D2H per pass, cascade at u_s
+//                              (lse.hpp:377-421, gls.hpp:336-380)
+//
+// Factors stay in HBM: the stacked fp32 (complex64) matrix M with T / R and
+// the packed reflectors, plus dense per-panel reflector blocks V_b and their
+// T_b for the blocked applies.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "large_common.cuh"
+#include "large_internal.h"
+#include "large_kernels.cuh"
+#include "../../include/mixedls_b200.h"
+#include "mlsb_internal.h"
+
+namespace mlsb {
+namespace lg {
+
+// ----------------------------------------------------------- glue kernels
+template <class WT>
+__global__ void k_rhs_scale(const WT* src, int n, double c, WT* dst, int* bad) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) {
+    WT v = src[i];
+    WT o;
+    if constexpr (tr<WT>::cplx) o = WT{v.x / c, v.y / c};
+    else o = v / c;
+    dst[i] = o;
+    if (bad && !finite_(o)) atomicOr(bad, 1);
+  }
+}
+template <class A, class B>
+__global__ void k_convert(const A* src, int n, B* dst) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) dst[i] = widen_to<B>(src[i]);
+}
+template <class T>
+__global__ void k_fill(T* x, int n, T v) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) x[i] = v;
+}
+template <class T>
+__global__ void k_copy(const T* x, int n, T* y) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) y[i] = x[i];
+}
+// y = a - b (elementwise), n entries
+template <class T>
+__global__ void k_sub(const T* a, const T* b, int n, T* y) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) y[i] = a[i] - b[i];
+}
+// y = a - (b + c)
+template <class T>
+__global__ void k_sub2(const T* a, const T* b, const T* c, int n, T* y) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) y[i] = a[i] - (b[i] + c[i]);
+}
+// y = a + (b - c)
+template <class T>
+__global__ void k_addsub(const T* a, const T* b, const T* c, int n, T* y) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) y[i] = a[i] + (b[i] - c[i]);
+}
+// y = a - b - c  (left to right)
+template <class T>
+__global__ void k_subsub(const T* a, const T* b, const T* c, int n, T* y) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) y[i] = a[i] - b[i] - c[i];
+}
+template <class T>
+__global__ void k_neg(T* x, int n) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) x[i] = -x[i];
+}
+// r_f = b_f - A_f x_f, A_f = fl(A * inv) in the factor precision (lse.hpp:353-355)
+template <class FT, class WT>
+__global__ void k_rowgemv_cast(const WT* A, int64_t lda, int rows, int cols, double inv,
+                               const FT* x, const FT* bf, FT* rf) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < rows; i += gridDim.x * KT) {
+    FT acc = zero<FT>();
+    for (int j = 0; j < cols; ++j) mac(acc, narrow<FT>(scale<WT>(inv, A[i + int64_t(j) * lda])), x[j]);
+    rf[i] = bf[i] - acc;
+  }
+}
+// max |x| over n entries (bits, NaN skipped)
+template <class T>
+__global__ void k_vmax(const T* x, int n, unsigned long long* bits) {
+  __shared__ double red[KT / 32];
+  double mx = 0.0;
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) {
+    const double t = mag(widen_to<typename tr<T>::wide>(x[i]));
+    mx = (mx < t) ? t : mx;
+  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m2 = 0.0;
+    for (int w = 0; w < KT / 32; ++w) m2 = fmax(m2, red[w]);
+    atomic_max_nonneg(bits, m2);
+  }
+}
+__device__ __forceinline__ double bits_or_one(const unsigned long long* bits) {
+  const double s = __longlong_as_double((long long)*bits);
+  return s == 0.0 ? 1.0 : s;
+}
+// out = narrow<CT>(x / s), s = max read from bits (or 1 when bits is null)
+template <class WT, class CT>
+__global__ void k_demote(const WT* x, int n, const unsigned long long* bits, CT* out) {
+  const double s = bits ? bits_or_one(bits) : 1.0;
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) {
+    const WT v = x[i];
+    WT q;
+    if constexpr (tr<WT>::cplx) q = WT{v.x / s, v.y / s};
+    else q = v / s;
+    out[i] = widen_to<CT>(q);
+  }
+}
+// y += s * widen(c)  (promote_with_scale + update, refine.hpp:117-119); flag non-finite
+template <class WT, class CT>
+__global__ void k_promote_add(WT* y, int n, const CT* c, const unsigned long long* bits, bool neg,
+                              int* bad) {
+  const double s = bits ? bits_or_one(bits) : 1.0;
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) {
+    WT cv = widen_to<WT>(c[i]);
+    if (neg) cv = -cv;
+    const WT v = y[i] + scale<WT>(s, cv);
+    y[i] = v;
+    if (!finite_(v)) atomicOr(bad, 1);
+  }
+}
+// y = s * widen(c)
+template <class WT, class CT>
+__global__ void k_promote(WT* y, int n, const CT* c, const unsigned long long* bits) {
+  const double s = bits ? bits_or_one(bits) : 1.0;
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) y[i] = scale<WT>(s, widen_to<WT>(c[i]));
+}
+template <class WT>
+__global__ void k_scale_out(const WT* x, int n, double f, WT* out) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) out[i] = scale<WT>(f, x[i]);
+}
+
+// ------------------------------------------------------- stop test kernel
+struct StopIn {
+  // vector segments whose squared norms are needed (up to 6), and which
+  // segments enter the demotion scale sigma
+  const void* seg[6];
+  int len[6];
+  int sigma_mask;  // bit s: segment s is a residual block
+};
+struct StopOut {
+  double nrm[6];
+  double sigma;
+  int bad;
+  int pad;
+};
+template <class WT>
+__global__ void __launch_bounds__(1024) k_stop(StopIn in, StopOut* out, unsigned long long* sbits,
+                                                const int* badflag) {
+  __shared__ double red[32][8];
+  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  for (int s = 0; s < 6; ++s) {
+    const WT* x = static_cast<const WT*>(in.seg[s]);
+    if (!x) continue;
+    for (int i = tid; i < in.len[s]; i += 1024) {
+      const WT v = x[i];
+      acc[s] += abs2d(v);
+      if ((in.sigma_mask >> s) & 1) {
+        const double t = mag(v);
+        acc[6] = (acc[6] < t) ? t : acc[6];
+      }
+    }
+  }
+  for (int k = 0; k < 7; ++k)
+    for (int o = 16; o; o >>= 1) {
+      const double t = __shfl_xor_sync(0xffffffffu, acc[k], o);
+      acc[k] = k < 6 ? acc[k] + t : fmax(acc[k], t);
+    }
+  if (l == 0)
+    for (int k = 0; k < 7; ++k) red[w][k] = acc[k];
+  __syncthreads();
+  if (tid == 0) {
+    double t[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int ww = 0; ww < 32; ++ww)
+      for (int k = 0; k < 7; ++k) t[k] = k < 6 ? t[k] + red[ww][k] : fmax(t[k], red[ww][k]);
+    for (int k = 0; k < 6; ++k) out->nrm[k] = sqrt(t[k]);
+    out->sigma = t[6];
+    out->bad = badflag ? *badflag : 0;
+    *sbits = (unsigned long long)__double_as_longlong(t[6]);
+  }
+}
+
+// ------------------------------------------------------------- host helpers
+static inline int nblk(int64_t n, int per = KT, int cap = 148 * 8) {
+  return int(std::max<int64_t>(1, std::min<int64_t>(cap, (n + per - 1) / per)));
+}
+
+struct Arena {
+  char* base = nullptr;
+  size_t used = 0, cap = 0;
+  cudaStream_t st = nullptr;
+  cudaError_t init(size_t bytes, cudaStream_t s) {
+    st = s;
+    cap = bytes;
+    return cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, s);
+  }
+  template <class T> T* take(size_t n) {
+    used = (used + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + used);
+    used += n * sizeof(T);
+    return used <= cap ? p : nullptr;
+  }
+  ~Arena() {
+    if (base) cudaFreeAsync(base, st);
+  }
+};
+
+template <class FT>
+struct Blk {
+  const FT* V;
+  int64_t ldv;
+  int L, nbk;
+  const FT* T;
+  int voff;
+};
+// F = P_0 P_1 ... P_last, P_b = I - V_b T_b V_b^H
+template <class FT>
+struct Fac {
+  std::vector<Blk<FT>> b;
+};
+
+template <class FT, class CT>
+static void apply_F(const Fac<FT>& F, bool herm, CT* x, CT* ypart, cudaStream_t st) {
+  const int nb = int(F.b.size());
+  for (int s = 0; s < nb; ++s) {
+    const Blk<FT>& b = F.b[herm ? s : nb - 1 - s];
+    const int rpc = 512;
+    const int ncta = (b.L + rpc - 1) / rpc;
+    k_wy_dot<FT, CT><<<ncta, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, x + b.voff, rpc, ypart);
+    k_wy_upd<FT, CT><<<ncta, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, b.T, herm, ypart, ncta, rpc,
+                                          x + b.voff);
+  }
+}
+
+// upper-triangular solve with U = M[r0:r0+k, c0:c0+k]; herm: U^H x = b
+template <class FT, class CT>
+static void trsv(const FT* M, int64_t ld, int64_t r0, int64_t c0, int k, bool herm, CT* x,
+                 cudaStream_t st) {
+  if (!herm) {
+    for (int i1 = k; i1 > 0; i1 -= 32) {
+      const int i0 = std::max(0, i1 - 32), bs = i1 - i0;
+      k_trsv_diag<FT, CT><<<1, 32, 0, st>>>(M, ld, r0, c0, i0, bs, false, x);
+      if (i0 > 0) k_trsv_off<FT, CT><<<nblk(i0), KT, 0, st>>>(M, ld, r0, c0, i0, bs, k, false, x);
+    }
+  } else {
+    for (int i0 = 0; i0 < k; i0 += 32) {
+      const int bs = std::min(32, k - i0);
+      k_trsv_diag<FT, CT><<<1, 32, 0, st>>>(M, ld, r0, c0, i0, bs, true, x);
+      if (i0 + bs < k)
+        k_trsv_off<FT, CT><<<nblk(k - i0 - bs, KT / 32), KT, 0, st>>>(M, ld, r0, c0, i0, bs, k, true, x);
+    }
+  }
+}
+
+template <class FT, class CT>
+static void gemv_n(const FT* M, int64_t ld, int r0, int rows, int c0, int cols, Mask mk, const CT* x,
+                   CT* y, cudaStream_t st) {
+  if (rows <= 0) return;
+  k_gemv_n<FT, CT><<<nblk(rows), KT, 0, st>>>(M, ld, r0, rows, c0, cols, mk, x, y);
+}
+template <class FT, class CT>
+static void gemv_h(const FT* M, int64_t ld, int r0, int rows, int c0, int cols, Mask mk, const CT* x,
+                   CT* y, cudaStream_t st) {
+  if (cols <= 0) return;
+  k_gemv_h<FT, CT><<<nblk(cols, KT / 32), KT, 0, st>>>(M, ld, r0, rows, c0, cols, mk, x, y);
+}
+
+template <class FT>
+static cudaError_t gemm(bool ha, bool hb, int Mr, int N, int K, double alpha, const FT* A,
+                        int64_t lda, const FT* B, int64_t ldb, double beta, FT* C, int64_t ldc,
+                        FT* work, size_t wn, cudaStream_t st) {
+  if constexpr (tr<FT>::cplx)
+    return gemm_c64(ha, hb, Mr, N, K, cf{float(alpha), 0.f}, A, lda, B, ldb, cf{float(beta), 0.f}, C,
+                    ldc, work, wn, st);
+  else
+    return gemm_f32(ha, hb, Mr, N, K, float(alpha), A, lda, B, ldb, float(beta), C, ldc, work, wn, st);
+}
+
+// ----------------------------------------------- blocked GRQ / GQR at u_f
+// QR of M[j0.., j0..] columns [0, k) over rows [0, rows), trailing columns up to cend
+template <class FT>
+static cudaError_t qr_stage(FT* M, int64_t ld, int rows, int k, int cend, FT* Vbuf, FT* Tbuf,
+                            FT* taus, FT* W, FT* W2, FT* work, size_t wn, Fac<FT>& F,
+                            cudaStream_t st) {
+  cudaError_t e;
+  size_t voff = 0;
+  for (int j0 = 0, b = 0; j0 < k; j0 += NB, ++b) {
+    const int nbk = std::min(NB, k - j0), L = rows - j0;
+    FT* V = Vbuf + voff;
+    FT* Tb = Tbuf + size_t(b) * NB * NB;
+    voff += size_t(L) * NB;
+    if ((e = panel_factor<FT>(M, ld, j0, j0, L, nbk, false, taus + j0, V, L, Tb, 0, st))) return e;
+    F.b.push_back(Blk<FT>{V, L, L, nbk, Tb, j0});
+    const int N2 = cend - j0 - nbk;
+    if (N2 <= 0) continue;
+    FT* C2 = M + j0 + int64_t(j0 + nbk) * ld;
+    // C2 := P^H C2 = C2 - V T^H (V^H C2)
+    if ((e = gemm<FT>(true, false, nbk, N2, L, 1.0, V, L, C2, ld, 0.0, W, NB, work, wn, st))) return e;
+    if ((e = gemm<FT>(true, false, nbk, N2, nbk, 1.0, Tb, NB, W, NB, 0.0, W2, NB, nullptr, 0, st)))
+      return e;
+    if ((e = gemm<FT>(false, false, L, N2, nbk, -1.0, V, L, W2, NB, 1.0, C2, ld, nullptr, 0, st)))
+      return e;
+  }
+  return cudaSuccess;
+}
+
+// RQ of the block rows [rb, rb+rr) x columns [cb, cb+cc) (rows bottom-up), applied
+// from the right to every row above; panels of NB rows from the bottom.
+template <class FT>
+static cudaError_t rq_stage(FT* M, int64_t ld, int rb, int rr, int cb, int cc, FT* Vbuf, FT* Tbuf,
+                            FT* taus, FT* W, FT* W2, FT* work, size_t wn, Fac<FT>& F,
+                            cudaStream_t st) {
+  cudaError_t e;
+  const int kk = std::min(rr, cc);
+  size_t voff = 0;
+  for (int r1 = kk, b = 0; r1 > 0; r1 -= NB, ++b) {
+    const int nbk = std::min(NB, r1);
+    // reflector j (0..kk-1): row rb + rr - kk + j, pivot column cb + cc - kk + j
+    const int jtop = r1 - 1;
+    const int64_t row_first = rb + rr - kk + jtop;
+    const int64_t pcmax = cb + cc - kk + jtop;
+    const int L = int(pcmax - cb + 1);
+    FT* V = Vbuf + voff;
+    FT* Tb = Tbuf + size_t(b) * NB * NB;
+    voff += size_t(L) * NB;
+    if ((e = panel_factor<FT>(M, ld, row_first, pcmax, L, nbk, true, taus + size_t(b) * NB, V, L, Tb,
+                              cb, st)))
+      return e;
+    F.b.push_back(Blk<FT>{V, L, L, nbk, Tb, 0});
+    const int above = int(row_first - (nbk - 1));  // rows [0, above)
+    if (above <= 0) continue;
+    FT* Ma = M + int64_t(cb) * ld;
+    // M_above := M_above P = M_above - (M_above V) T V^H
+    if ((e = gemm<FT>(false, false, above, nbk, L, 1.0, Ma, ld, V, L, 0.0, W, above, work, wn, st)))
+      return e;
+    if ((e = gemm<FT>(false, false, above, nbk, nbk, 1.0, W, above, Tb, NB, 0.0, W2, above, nullptr, 0,
+                      st)))
+      return e;
+    if ((e = gemm<FT>(false, true, above, L, nbk, -1.0, W2, above, V, L, 1.0, Ma, ld, nullptr, 0, st)))
+      return e;
+  }
+  return cudaSuccess;
+}
+
+// --------------------------------------------------------------- driver
+template <class FT, class WT, class CT>
+static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
+  const bool lse = P.kind == KIND_LSE;
+  const int m = int(P.m), n = int(P.n), p = int(P.p);
+  const int R = lse ? m + p : n, C = lse ? n : m + p;
+  const int64_t ld = R;
+  const int kq = lse ? p : std::min(n, p);  // RQ reflectors
+  const int kz = lse ? std::min(m, n) : m;  // QR reflectors
+  const int nbz = (kz + NB - 1) / NB, nbq = (kq + NB - 1) / NB;
+  const int ntr = (R + RTR - 1) / RTR, ntc = (C + RTC - 1) / RTC;
+  const int L = std::max(R, C);
+  const size_t wn = size_t(NB) * std::max(R, C) * 64;  // split-K partials
+  const bool lows = sizeof(CT) == sizeof(FT);
+
+  Arena ar;
+  const size_t bytes = sizeof(FT) * (size_t(R) * C + size_t(nbz) * R * NB + size_t(nbq) * C * NB +
+                                     size_t(nbz + nbq) * NB * NB + size_t(C + R) + 2 * size_t(R) * NB +
+                                     wn + 8 * size_t(L)) +
+                       sizeof(WT) * (size_t(R) * (6 + ntc) + size_t(C) * (5 + ntr)) +
+                       sizeof(CT) * (10 * size_t(L) + 32 * 64) + 64 * 1024 + 64 * 256;
+  cudaError_t e = ar.init(bytes + bytes / 4 + (1 << 20), st);
+  if (e) return MLSB_ERR_CUDA;
+  FT* M = ar.take<FT>(size_t(R) * C);
+  FT* VZ = ar.take<FT>(size_t(nbz) * R * NB);
+  FT* VQ = ar.take<FT>(size_t(nbq) * C * NB);
+  FT* TZ = ar.take<FT>(size_t(nbz) * NB * NB);
+  FT* TQ = ar.take<FT>(size_t(nbq) * NB * NB);
+  FT* tauZ = ar.take<FT>(C);
+  FT* tauQ = ar.take<FT>(size_t(nbq) * NB + R);
+  FT* W = ar.take<FT>(size_t(L) * NB);
+  FT* W2 = ar.take<FT>(size_t(L) * NB);
+  FT* gw = ar.take<FT>(wn);
+  FT* fv[8];
+  for (int i = 0; i < 8; ++i) fv[i] = ar.take<FT>(L);
+  WT* rinit = ar.take<WT>(R);
+  WT* rrow = ar.take<WT>(R);  // row initialisers of the current pass
+  WT* rout = ar.take<WT>(R);
+  WT* sw = ar.take<WT>(R);
+  WT* wvec = ar.take<WT>(R);
+  WT* cinit = ar.take<WT>(C);
+  WT* cout = ar.take<WT>(C);
+  WT* su = ar.take<WT>(C);
+  WT* rpart = ar.take<WT>(size_t(ntc) * R);
+  WT* cpart = ar.take<WT>(size_t(ntr) * C);
+  WT* gvec = ar.take<WT>(C);
+  CT* cv[10];
+  for (int i = 0; i < 10; ++i) cv[i] = ar.take<CT>(L);
+  CT* ypart = ar.take<CT>(32 * 64);
+  char* small = ar.take<char>(64 * 1024);
+  if (!small) return MLSB_ERR_CUDA;
+  unsigned long long* bits = reinterpret_cast<unsigned long long*>(small);  // [8]
+  double* parts = reinterpret_cast<double*>(small + 1024);                   // [>= 2*grid]
+  double* nsum = reinterpret_cast<double*>(small + 32 * 1024);               // [8]
+  int* flags = reinterpret_cast<int*>(small + 33 * 1024);                    // [8]
+  StopOut* so = reinterpret_cast<StopOut*>(small + 34 * 1024);
+  cudaMemsetAsync(small, 0, 64 * 1024, st);
+
+  const WT* gA = static_cast<const WT*>(P.A);
+  const WT* gB = static_cast<const WT*>(P.B);
+  const WT* gb = static_cast<const WT*>(P.b);
+  const WT* gd = static_cast<const WT*>(P.d);
+  cudaEvent_t ev[8];
+  for (auto& x : ev) cudaEventCreate(&x);
+  cudaEventRecord(ev[0], st);
+
+  // ---------------------------------------------------------- pre-scaling
+  const int rows1 = lse ? m : n, cols1 = lse ? n : m;  // A (LSE) / W (GLS)
+  const int rows2 = lse ? p : n, cols2 = lse ? n : p;  // B / V
+  const int grid = 148 * 4;
+  k_maxabs<WT><<<grid, KT, 0, st>>>(gA, P.lda, rows1, cols1, bits + 0);
+  k_maxabs<WT><<<grid, KT, 0, st>>>(gB, P.ldb, rows2, cols2, bits + 1);
+  if (lse) k_maxabs<WT><<<grid, KT, 0, st>>>(gb, m, m, 1, bits + 2);
+  else k_maxabs<WT><<<grid, KT, 0, st>>>(gd, n, n, 1, bits + 2);
+  unsigned long long hb[3];
+  cudaMemcpyAsync(hb, bits, sizeof(hb), cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;
+  auto asd = [](unsigned long long b) {
+    double v;
+    memcpy(&v, &b, 8);
+    return v == 0.0 ? 1.0 : v;
+  };
+  const double sA = asd(hb[0]), sB = asd(hb[1]), c1 = asd(hb[2]);
+  const double c2 = lse ? sB * c1 / sA : c1;  // LSE c_d = s_B c_b / s_A ; GLS c_d
+  // right-hand sides (exact division, lse.hpp:326-329)
+  if (lse) {
+    k_rhs_scale<WT><<<nblk(m), KT, 0, st>>>(gb, m, c1, rinit, nullptr);
+    k_rhs_scale<WT><<<nblk(p), KT, 0, st>>>(gd, p, c2, rinit + m, flags + 0);
+  } else {
+    k_rhs_scale<WT><<<nblk(n), KT, 0, st>>>(gd, n, c2, rinit, nullptr);
+  }
+  // fp32 factor input and ||A_s||_F, ||B_s||_F
+  if (lse) {
+    k_cast<FT, WT><<<grid, KT, 0, st>>>(gA, P.lda, m, n, 1.0 / sA, M, ld, parts);
+    k_sum_parts<<<1, 32, 0, st>>>(parts, grid, nsum + 0);
+    k_cast<FT, WT><<<grid, KT, 0, st>>>(gB, P.ldb, p, n, 1.0 / sB, M + m, ld, parts + grid);
+    k_sum_parts<<<1, 32, 0, st>>>(parts + grid, grid, nsum + 1);
+  } else {
+    k_cast<FT, WT><<<grid, KT, 0, st>>>(gA, P.lda, n, m, 1.0 / sA, M, ld, parts);
+    k_sum_parts<<<1, 32, 0, st>>>(parts, grid, nsum + 0);
+    k_cast<FT, WT><<<grid, KT, 0, st>>>(gB, P.ldb, n, p, 1.0 / sB, M + int64_t(m) * ld, ld, parts + grid);
+    k_sum_parts<<<1, 32, 0, st>>>(parts + grid, grid, nsum + 1);
+  }
+  // ||b_s||, ||d_s|| through the stop kernel
+  {
+    StopIn si{};
+    if (lse) {
+      si.seg[0] = rinit;
+      si.len[0] = m;
+      si.seg[1] = rinit + m;
+      si.len[1] = p;
+    } else {
+      si.seg[0] = rinit;
+      si.len[0] = n;
+    }
+    k_stop<WT><<<1, 1024, 0, st>>>(si, so, bits + 3, flags + 0);
+  }
+  double hn[2];
+  StopOut hso;
+  cudaMemcpyAsync(hn, nsum, sizeof(hn), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&hso, so, sizeof(hso), cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;
+  if (lse && hso.bad) {
+    out->err = MLSB_ERR_INVALID_INPUT;
+    return MLSB_OK;
+  }
+  const double nA = sqrt(hn[0]), nB = sqrt(hn[1]);
+  const double nb_ = lse ? hso.nrm[0] : 0.0, nd = lse ? hso.nrm[1] : hso.nrm[0];
+  cudaEventRecord(ev[1], st);
+
+  // ---------------------------------------------------------- GRQ / GQR
+  Fac<FT> FZ, FQ;  // QR factor (Z for LSE, Q for GLS) / RQ factor (Q^H for LSE, Z^H for GLS)
+  if (lse) {
+    if ((e = rq_stage<FT>(M, ld, m, p, 0, n, VQ, TQ, tauQ, W, W2, gw, wn, FQ, st))) return MLSB_ERR_CUDA;
+    if ((e = qr_stage<FT>(M, ld, m, kz, n, VZ, TZ, tauZ, W, W2, gw, wn, FZ, st))) return MLSB_ERR_CUDA;
+  } else {
+    if ((e = qr_stage<FT>(M, ld, n, kz, m + p, VZ, TZ, tauZ, W, W2, gw, wn, FZ, st))) return MLSB_ERR_CUDA;
+    if ((e = rq_stage<FT>(M, ld, 0, n, m, p, VQ, TQ, tauQ, W, W2, gw, wn, FQ, st))) return MLSB_ERR_CUDA;
+  }
+  // zero pivots in the order of the reference's first failing trsv
+  // (LSE: R at lse.hpp:53, then T11 at :60; GLS: T22 at gls.hpp:55, then R at :61)
+  const int kl = lse ? n - p : p - n + m;  // LSE: size of T11 ; GLS: column split of T
+  {
+    k_fill<int><<<1, 32, 0, st>>>(flags + 1, 2, -1);
+    if (lse) {
+      k_pivot_scan<FT><<<nblk(p), KT, 0, st>>>(M, ld, m, n - p, p, flags + 1);
+      k_pivot_scan<FT><<<nblk(kl), KT, 0, st>>>(M, ld, 0, 0, kl, flags + 2);
+    } else {
+      k_pivot_scan<FT><<<nblk(n - m), KT, 0, st>>>(M, ld, m, m + kl, n - m, flags + 1);
+      k_pivot_scan<FT><<<nblk(m), KT, 0, st>>>(M, ld, 0, 0, m, flags + 2);
+    }
+    int hf[2];
+    cudaMemcpyAsync(hf, flags + 1, sizeof(hf), cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;
+    if (hf[0] >= 0 || hf[1] >= 0) {
+      out->err = MLSB_ERR_SINGULAR;
+      out->sing = hf[0] >= 0 ? hf[0] : hf[1];
+      return MLSB_OK;
+    }
+  }
+  cudaEventRecord(ev[2], st);
+
+  // ---------------------------------------------------------- initial solve at u_f
+  FT* ypf = reinterpret_cast<FT*>(ypart);
+  const Mask none{0, 0, 0};
+  if (lse) {
+    const int k = kl;
+    FT *bf = fv[0], *y2 = fv[1], *c = fv[2], *t4 = fv[3], *y = fv[4], *rf = fv[5], *gf = fv[6];
+    k_convert<WT, FT><<<nblk(m), KT, 0, st>>>(rinit, m, bf);
+    k_convert<WT, FT><<<nblk(p), KT, 0, st>>>(rinit + m, p, y2);
+    k_copy<FT><<<nblk(m), KT, 0, st>>>(bf, m, c);
+    trsv<FT, FT>(M, ld, m, n - p, p, false, y2, st);      // R y2 = d
+    apply_F<FT, FT>(FZ, true, c, ypf, st);                   // c = Z^H b
+    gemv_n<FT, FT>(M, ld, 0, k, k, p, none, y2, t4, st);    // T12 y2
+    k_sub<FT><<<nblk(k), KT, 0, st>>>(c, t4, k, y);
+    k_copy<FT><<<nblk(p), KT, 0, st>>>(y2, p, y + k);
+    trsv<FT, FT>(M, ld, 0, 0, k, false, y, st);             // T11 y1 = c1 - T12 y2
+    apply_F<FT, FT>(FQ, false, y, ypf, st);                  // x = Q^H [y1; y2]  (F_Q = Q^H)
+    k_rowgemv_cast<FT, WT><<<nblk(m), KT, 0, st>>>(gA, P.lda, m, n, 1.0 / sA, y, bf, rf);
+    k_convert<FT, WT><<<nblk(n), KT, 0, st>>>(y, n, su);
+    k_convert<FT, WT><<<nblk(m), KT, 0, st>>>(rf, m, sw);
+    // solve_v (lse.hpp:156-165): g = A^H r at u_r, sigma, Q g, R^H v = g(n-p:n)
+    {
+      Stack<WT> S{gA, gB, P.lda, P.ldb, m, true, 1.0 / sA, 1.0 / sB};
+      k_fill<WT><<<nblk(n), KT, 0, st>>>(gvec, n, zero<WT>());
+      dim3 g2((m + RTR - 1) / RTR, ntc);
+      k_resid_tile<WT><<<g2, KT, 0, st>>>(S, m, n, gvec, sw, rpart, cpart);
+      k_resid_reduce<WT><<<nblk(m + n), KT, 0, st>>>(m, n, ntc, (m + RTR - 1) / RTR, rpart, cpart, rinit,
+                                                     nullptr, rout, cout);
+      cudaMemsetAsync(bits + 4, 0, 8, st);
+      k_vmax<WT><<<nblk(n), KT, 0, st>>>(cout, n, bits + 4);
+      k_demote<WT, FT><<<nblk(n), KT, 0, st>>>(cout, n, bits + 4, gf);
+      apply_F<FT, FT>(FQ, true, gf, ypf, st);                // Q g = F_Q^H g
+      trsv<FT, FT>(M, ld, m, n - p, p, true, gf + (n - p), st);
+      k_promote<WT, FT><<<nblk(p), KT, 0, st>>>(sw + m, p, gf + (n - p), bits + 4);
+    }
+  } else {
+    const int nm = n - m;
+    const int kk = std::min(n, p);
+    FT *c = fv[0], *rhs = fv[1], *yv = fv[2], *g = fv[3], *zq = fv[4], *t = fv[5];
+    k_convert<WT, FT><<<nblk(n), KT, 0, st>>>(rinit, n, c);
+    apply_F<FT, FT>(FZ, true, c, ypf, st);                   // c = Q^H d
+    trsv<FT, FT>(M, ld, m, m + kl, nm, false, c + m, st);   // T22 s2 = c2
+    gemv_n<FT, FT>(M, ld, 0, m, m + kl, nm, none, c + m, t, st);
+    k_sub<FT><<<nblk(m), KT, 0, st>>>(c, t, m, rhs);
+    trsv<FT, FT>(M, ld, 0, 0, m, false, rhs, st);           // R x = c1 - T12 s2
+    k_fill<FT><<<nblk(kl), KT, 0, st>>>(yv, kl, zero<FT>());
+    k_copy<FT><<<nblk(nm), KT, 0, st>>>(c + m, nm, yv + kl);
+    apply_F<FT, FT>(FQ, false, yv, ypf, st);                 // y = Z^H s  (F_Z = Z^H)
+    // init_z: g = Z y, T22^H v = g2, z = Q [0; v]
+    k_copy<FT><<<nblk(p), KT, 0, st>>>(yv, p, g);
+    apply_F<FT, FT>(FQ, true, g, ypf, st);                   // Z y = F^H y
+    trsv<FT, FT>(M, ld, m, m + kl, nm, true, g + kl, st);
+    k_fill<FT><<<nblk(m), KT, 0, st>>>(zq, m, zero<FT>());
+    k_copy<FT><<<nblk(nm), KT, 0, st>>>(g + kl, nm, zq + m);
+    apply_F<FT, FT>(FZ, false, zq, ypf, st);                 // z = Q zq
+    k_convert<FT, WT><<<nblk(m), KT, 0, st>>>(rhs, m, su);
+    k_convert<FT, WT><<<nblk(p), KT, 0, st>>>(yv, p, su + m);
+    k_convert<FT, WT><<<nblk(n), KT, 0, st>>>(zq, n, sw);
+    (void)kk;
+  }
+  if ((e = cudaGetLastError())) return MLSB_ERR_CUDA;
+  cudaEventRecord(ev[3], st);
+
+  // ---------------------------------------------------------- refinement loop
+  Stack<WT> S{gA, gB, P.lda, P.ldb, m, lse, 1.0 / sA, 1.0 / sB};
+  double best = INFINITY;
+  int status = 1;
+  int64_t pass = 0;
+  out->hist.clear();
+  for (pass = 1; pass <= P.maxit; ++pass) {
+    // row initialisers and weights of this pass
+    if (lse) {
+      k_sub<WT><<<nblk(m), KT, 0, st>>>(rinit, sw, m, rrow);                  // b - r
+      k_copy<WT><<<nblk(p), KT, 0, st>>>(rinit + m, p, rrow + m);             // d
+      k_copy<WT><<<nblk(R), KT, 0, st>>>(sw, R, wvec);
+      k_neg<WT><<<nblk(m), KT, 0, st>>>(wvec, m);                              // [-r; v]
+      k_fill<WT><<<nblk(C), KT, 0, st>>>(cinit, C, zero<WT>());
+    } else {
+      k_copy<WT><<<nblk(n), KT, 0, st>>>(rinit, n, rrow);                      // d
+      k_copy<WT><<<nblk(n), KT, 0, st>>>(sw, n, wvec);                         // z
+      k_fill<WT><<<nblk(m), KT, 0, st>>>(cinit, m, zero<WT>());
+      k_copy<WT><<<nblk(p), KT, 0, st>>>(su + m, p, cinit + m);
+      k_neg<WT><<<nblk(p), KT, 0, st>>>(cinit + m, p);                          // [0; -y]
+    }
+    dim3 g2(ntr, ntc);
+    k_resid_tile<WT><<<g2, KT, 0, st>>>(S, R, C, su, wvec, rpart, cpart);
+    k_resid_reduce<WT><<<nblk(R + C), KT, 0, st>>>(R, C, ntc, ntr, rpart, cpart, rrow, cinit, rout, cout);
+    StopIn si{};
+    if (lse) {  // f1, f2, f3 | r, v, x
+      si.seg[0] = rout;       si.len[0] = m;
+      si.seg[1] = rout + m;   si.len[1] = p;
+      si.seg[2] = cout;       si.len[2] = n;
+      si.seg[3] = sw;         si.len[3] = m;
+      si.seg[4] = sw + m;     si.len[4] = p;
+      si.seg[5] = su;         si.len[5] = n;
+    } else {    // f1 = cout[m:], f2 = rout, f3 = cout[:m] | x, y, z
+      si.seg[0] = cout + m;   si.len[0] = p;
+      si.seg[1] = rout;       si.len[1] = n;
+      si.seg[2] = cout;       si.len[2] = m;
+      si.seg[3] = su;         si.len[3] = m;
+      si.seg[4] = su + m;     si.len[4] = p;
+      si.seg[5] = sw;         si.len[5] = n;
+    }
+    si.sigma_mask = 7;
+    k_stop<WT><<<1, 1024, 0, st>>>(si, so, bits + 5, flags + 3);
+    cudaMemcpyAsync(&hso, so, sizeof(hso), cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;
+    if (hso.bad) {  // the previous update went non-finite (lse.hpp:417-420)
+      status = 2;
+      --pass;
+      break;
+    }
+    const double g1 = hso.nrm[0], g2n = hso.nrm[1], g3 = hso.nrm[2];
+    const double s3 = hso.nrm[3], s4 = hso.nrm[4], s5 = hso.nrm[5];
+    double d1, d2, d3;
+    if (lse) {  // lse.hpp:272-277, history :384-385
+      d1 = nb_ + s3 + nA * s5;
+      d2 = nd + nB * s5;
+      d3 = nA * s3 + nB * s4;
+      out->hist.push_back(g1 * c1);
+      out->hist.push_back(g2n * c2);
+      out->hist.push_back(g3 * sA * c1);
+    } else {    // gls.hpp:246-251, history :343-344
+      d1 = s4 + nB * s5;
+      d2 = nd + nA * s3 + nB * s4;
+      d3 = nA * s5;
+      out->hist.push_back(g1 * c2 / sB);
+      out->hist.push_back(g2n * c2);
+      out->hist.push_back(g3 * sA * c2 / (sB * sB));
+    }
+    const double tol = P.tol;
+    if (g1 <= tol * d1 && g2n <= tol * d2 && g3 <= tol * d3) {
+      status = 0;
+      break;
+    }
+    auto ratio = [](double num, double den) {
+      if (den > 0.0) return num / den;
+      return num == 0.0 ? 0.0 : INFINITY;
+    };
+    const double r1 = ratio(g1, d1), r2 = ratio(g2n, d2), r3 = ratio(g3, d3);
+    const double t12 = r1 < r2 ? r2 : r1, sm = t12 < r3 ? r3 : t12;
+    if (!std::isfinite(sm)) {
+      status = 2;
+      break;
+    }
+    if (sm < best) best = sm;
+    if (sm >= 1e4 * best && best > 0.0) {
+      status = 2;
+      break;
+    }
+
+    // ---- correction at u_s (demotion by one sigma, refine.hpp:103-107)
+    const unsigned long long* sb = lows ? bits + 5 : nullptr;
+    if (lse) {  // Algorithm 1 (lse.hpp:83-128)
+      const int k = kl;
+      CT *u = cv[0], *w = cv[1], *y2 = cv[2], *q1 = cv[3], *t4 = cv[4], *y = cv[5], *dr = cv[6],
+         *tq = cv[7];
+      k_demote<WT, CT><<<nblk(n), KT, 0, st>>>(cout, n, sb, u);
+      k_demote<WT, CT><<<nblk(m), KT, 0, st>>>(rout, m, sb, w);
+      k_demote<WT, CT><<<nblk(p), KT, 0, st>>>(rout + m, p, sb, y2);
+      apply_F<FT, CT>(FQ, true, u, ypart, st);                  // u = Q f3 = F^H f3
+      apply_F<FT, CT>(FZ, true, w, ypart, st);                  // w = Z^H f1
+      trsv<FT, CT>(M, ld, m, n - p, p, false, y2, st);          // R y2 = f2
+      k_copy<CT><<<nblk(k), KT, 0, st>>>(u, k, q1);
+      trsv<FT, CT>(M, ld, 0, 0, k, true, q1, st);               // T11^H q1 = u1
+      gemv_n<FT, CT>(M, ld, 0, k, k, p, none, y2, t4, st);       // T12 y2
+      gemv_n<FT, CT>(M, ld, k, m - k, k, p, Mask{1, 0, 0}, y2, t4 + k, st);  // T22 y2
+      k_subsub<CT><<<nblk(k), KT, 0, st>>>(w, q1, t4, k, y);      // y1 rhs = w1 - q1 - T12 y2
+      k_copy<CT><<<nblk(k), KT, 0, st>>>(q1, k, w);               // q = [q1; w2 - T22 y2]
+      k_sub<CT><<<nblk(m - k), KT, 0, st>>>(w + k, t4 + k, m - k, w + k);
+      k_copy<CT><<<nblk(m), KT, 0, st>>>(w, m, dr);
+      k_copy<CT><<<nblk(p), KT, 0, st>>>(y2, p, y + k);
+      trsv<FT, CT>(M, ld, 0, 0, k, false, y, st);               // T11 y1 = ...
+      apply_F<FT, CT>(FQ, false, y, ypart, st);                 // dx = Q^H y = F y
+      apply_F<FT, CT>(FZ, false, dr, ypart, st);                // dr = Z q = F q
+      gemv_h<FT, CT>(M, ld, 0, k, k, p, none, w, t4, st);        // T12^H q1
+      gemv_h<FT, CT>(M, ld, k, m - k, k, p, Mask{1, 0, 0}, w + k, tq, st);  // T22^H q2
+      k_addsub<CT><<<nblk(p), KT, 0, st>>>(t4, tq, u + k, p, t4);  // s = T12^H q1 + (T22^H q2 - u2)
+      trsv<FT, CT>(M, ld, m, n - p, p, true, t4, st);            // R^H dv = s
+      k_promote_add<WT, CT><<<nblk(m), KT, 0, st>>>(sw, m, dr, sb, false, flags + 3);
+      k_promote_add<WT, CT><<<nblk(p), KT, 0, st>>>(sw + m, p, t4, sb, false, flags + 3);
+      k_promote_add<WT, CT><<<nblk(n), KT, 0, st>>>(su, n, y, sb, false, flags + 3);
+    } else {    // Algorithm 3 (gls.hpp:106-154)
+      const int nm = n - m, kp = kl;
+      const int kk = std::min(n, p);
+      const Mask rqm{2, n - kk, m + (p - kk)};
+      CT *u = cv[0], *w = cv[1], *h1 = cv[2], *g2 = cv[3], *t4 = cv[4], *r2 = cv[5], *g = cv[6],
+         *r1v = cv[7], *tq = cv[8], *hh = cv[9];
+      k_demote<WT, CT><<<nblk(n), KT, 0, st>>>(rout, n, sb, u);       // f2
+      k_demote<WT, CT><<<nblk(p), KT, 0, st>>>(cout + m, p, sb, w);   // f1
+      k_demote<WT, CT><<<nblk(m), KT, 0, st>>>(cout, m, sb, h1);      // f3
+      apply_F<FT, CT>(FZ, true, u, ypart, st);                        // u = Q^H f2
+      apply_F<FT, CT>(FQ, true, w, ypart, st);                        // w = Z f1 = F^H f1
+      trsv<FT, CT>(M, ld, 0, 0, m, true, h1, st);                     // R^H h1 = f3
+      k_copy<CT><<<nblk(nm), KT, 0, st>>>(u + m, nm, g2);
+      trsv<FT, CT>(M, ld, m, m + kp, nm, false, g2, st);              // T22 g2 = u2
+      gemv_h<FT, CT>(M, ld, 0, m, m + kp, nm, none, h1, t4, st);       // T12^H h1
+      gemv_h<FT, CT>(M, ld, 0, m, m, kp, rqm, h1, tq, st);             // T11^H h1
+      k_subsub<CT><<<nblk(nm), KT, 0, st>>>(w + kp, g2, t4, nm, r2);  // w2 - g2 - T12^H h1
+      k_sub<CT><<<nblk(kp), KT, 0, st>>>(w, tq, kp, g);               // g1 = w1 - T11^H h1
+      k_copy<CT><<<nblk(nm), KT, 0, st>>>(g2, nm, g + kp);
+      trsv<FT, CT>(M, ld, m, m + kp, nm, true, r2, st);               // T22^H h2 = ...
+      k_copy<CT><<<nblk(p), KT, 0, st>>>(g, p, hh);
+      apply_F<FT, CT>(FQ, false, hh, ypart, st);                       // dy = Z^H g = F g
+      gemv_n<FT, CT>(M, ld, 0, m, m, kp, rqm, g, t4, st);              // T11 g1
+      gemv_n<FT, CT>(M, ld, 0, m, m + kp, nm, none, g2, tq, st);       // T12 g2
+      k_sub2<CT><<<nblk(m), KT, 0, st>>>(u, t4, tq, m, r1v);          // u1 - (T11 g1 + T12 g2)
+      trsv<FT, CT>(M, ld, 0, 0, m, false, r1v, st);                   // R dx = ...
+      k_copy<CT><<<nblk(m), KT, 0, st>>>(h1, m, u);
+      k_copy<CT><<<nblk(nm), KT, 0, st>>>(r2, nm, u + m);
+      apply_F<FT, CT>(FZ, false, u, ypart, st);                        // Q [h1; h2]
+      k_promote_add<WT, CT><<<nblk(m), KT, 0, st>>>(su, m, r1v, sb, false, flags + 3);
+      k_promote_add<WT, CT><<<nblk(p), KT, 0, st>>>(su + m, p, hh, sb, false, flags + 3);
+      k_promote_add<WT, CT><<<nblk(n), KT, 0, st>>>(sw, n, u, sb, true, flags + 3);  // dz = -Q h
+    }
+    if ((e = cudaGetLastError())) return MLSB_ERR_CUDA;
+  }
+  if (pass > P.maxit) pass = P.maxit;
+  if (status == 1) {
+    // maxit reached: the last update's non-finite check (lse.hpp:417-420) has
+    // not been read by a stop test yet
+    int hbad = 0;
+    cudaMemcpyAsync(&hbad, flags + 3, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;
+    if (hbad) status = 2;
+  }
+  cudaEventRecord(ev[4], st);
+  // ---------------------------------------------------------- unscale outputs
+  if (lse) {  // lse.hpp:424-426
+    k_scale_out<WT><<<nblk(n), KT, 0, st>>>(su, n, c1 / sA, static_cast<WT*>(P.x));
+    k_scale_out<WT><<<nblk(m), KT, 0, st>>>(sw, m, c1, static_cast<WT*>(P.r));
+    k_scale_out<WT><<<nblk(p), KT, 0, st>>>(sw + m, p, sA * c1 / sB, static_cast<WT*>(P.v));
+  } else {    // gls.hpp:382-384
+    k_scale_out<WT><<<nblk(m), KT, 0, st>>>(su, m, c2 / sA, static_cast<WT*>(P.x));
+    k_scale_out<WT><<<nblk(p), KT, 0, st>>>(su + m, p, c2 / sB, static_cast<WT*>(P.r));
+    k_scale_out<WT><<<nblk(n), KT, 0, st>>>(sw, n, c2 / (sB * sB), static_cast<WT*>(P.v));
+  }
+  cudaEventRecord(ev[5], st);
+  if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;
+  float ms[5];
+  for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
+  out->phases[5] = (ms[0] + ms[4]) * 1e-3;  // other
+  out->phases[0] = ms[1] * 1e-3;            // factorization
+  out->phases[1] = ms[2] * 1e-3;            // init
+  out->phases[2] = ms[3] * 1e-3;            // residual + correction (loop)
+  out->phases[3] = 0.0;
+  out->phases[4] = 0.0;
+  for (auto& x : ev) cudaEventDestroy(x);
+  out->status = status;
+  out->iters = pass;
+  out->err = MLSB_OK;
+  return MLSB_OK;
+}
+
+int large_solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
+  if (P.u_f != 0 || P.u_r == 2) return MLSB_ERR_UNSUPPORTED;
+  if (P.cplx) {
+    if (P.u_s != 0) return solve<cf, cd, cd>(P, st, out);
+    return solve<cf, cd, cf>(P, st, out);
+  }
+  if (P.u_s != 0) return solve<float, double, double>(P, st, out);
+  return solve<float, double, float>(P, st, out);
+}
+
+}  // namespace lg
+}  // namespace mlsb

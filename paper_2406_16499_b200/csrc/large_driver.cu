@@ -240,7 +240,9 @@ static void apply_F(const Fac<FT>& F, bool herm, CT* x, CT* ypart, cudaStream_t 
   const int nb = int(F.b.size());
   for (int s = 0; s < nb; ++s) {
     const Blk<FT>& b = F.b[herm ? s : nb - 1 - s];
-    const int rpc = 512;
+    // ~128 CTAs per apply, rows per CTA a multiple of 32
+    int rpc = ((b.L + 127) / 128 + 31) / 32 * 32;
+    if (rpc < 64) rpc = 64;
     const int ncta = (b.L + rpc - 1) / rpc;
     k_wy_dot<FT, CT><<<ncta, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, x + b.voff, rpc, ypart);
     k_wy_upd<FT, CT><<<ncta, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, b.T, herm, ypart, ncta, rpc,
@@ -293,31 +295,77 @@ static cudaError_t gemm(bool ha, bool hb, int Mr, int N, int K, double alpha, co
 }
 
 // ----------------------------------------------- blocked GRQ / GQR at u_f
-// QR of M[j0.., j0..] columns [0, k) over rows [0, rows), trailing columns up to cend
+// Look-ahead: after panel b, the columns (rows, for RQ) of panel b+1 are
+// updated first; panel b+1 is then factored by its cluster on the
+// high-priority stream `s2` while the remaining trailing update of panel b
+// (the big GEMM) runs on `st` over the other SMs.
+struct Streams {
+  cudaStream_t st, s2;
+  cudaEvent_t ev_upd, ev_pan;
+};
+
+// C2 := P^H C2 = C2 - V T^H (V^H C2) for C2 = M[j0:j0+L, c0:c0+nc]
+template <class FT>
+static cudaError_t qr_update(FT* M, int64_t ld, int j0, int L, int nbk, int c0, int nc, const FT* V,
+                             const FT* Tb, FT* W, FT* W2, FT* work, size_t wn, cudaStream_t st) {
+  if (nc <= 0) return cudaSuccess;
+  cudaError_t e;
+  FT* C2 = M + j0 + int64_t(c0) * ld;
+  if ((e = gemm<FT>(true, false, nbk, nc, L, 1.0, V, L, C2, ld, 0.0, W, NB, work, wn, st))) return e;
+  if ((e = gemm<FT>(true, false, nbk, nc, nbk, 1.0, Tb, NB, W, NB, 0.0, W2, NB, nullptr, 0, st))) return e;
+  return gemm<FT>(false, false, L, nc, nbk, -1.0, V, L, W2, NB, 1.0, C2, ld, nullptr, 0, st);
+}
+
+// QR of M[0:rows, 0:k] (columns), trailing columns up to cend
 template <class FT>
 static cudaError_t qr_stage(FT* M, int64_t ld, int rows, int k, int cend, FT* Vbuf, FT* Tbuf,
                             FT* taus, FT* W, FT* W2, FT* work, size_t wn, Fac<FT>& F,
-                            cudaStream_t st) {
+                            const Streams& S) {
   cudaError_t e;
-  size_t voff = 0;
-  for (int j0 = 0, b = 0; j0 < k; j0 += NB, ++b) {
-    const int nbk = std::min(NB, k - j0), L = rows - j0;
-    FT* V = Vbuf + voff;
-    FT* Tb = Tbuf + size_t(b) * NB * NB;
-    voff += size_t(L) * NB;
-    if ((e = panel_factor<FT>(M, ld, j0, j0, L, nbk, false, taus + j0, V, L, Tb, 0, st))) return e;
-    F.b.push_back(Blk<FT>{V, L, L, nbk, Tb, j0});
-    const int N2 = cend - j0 - nbk;
-    if (N2 <= 0) continue;
-    FT* C2 = M + j0 + int64_t(j0 + nbk) * ld;
-    // C2 := P^H C2 = C2 - V T^H (V^H C2)
-    if ((e = gemm<FT>(true, false, nbk, N2, L, 1.0, V, L, C2, ld, 0.0, W, NB, work, wn, st))) return e;
-    if ((e = gemm<FT>(true, false, nbk, N2, nbk, 1.0, Tb, NB, W, NB, 0.0, W2, NB, nullptr, 0, st)))
-      return e;
-    if ((e = gemm<FT>(false, false, L, N2, nbk, -1.0, V, L, W2, NB, 1.0, C2, ld, nullptr, 0, st)))
-      return e;
+  const int np = (k + NB - 1) / NB;
+  std::vector<size_t> voff(np + 1, 0);
+  for (int b = 0; b < np; ++b) voff[b + 1] = voff[b] + size_t(rows - b * NB) * NB;
+  auto V_of = [&](int b) { return Vbuf + voff[b]; };
+  auto T_of = [&](int b) { return Tbuf + size_t(b) * NB * NB; };
+  if (np == 0) return cudaSuccess;
+  if ((e = panel_factor<FT>(M, ld, 0, 0, rows, std::min(NB, k), false, taus, V_of(0), rows, T_of(0), 0,
+                            S.st)))
+    return e;
+  for (int b = 0; b < np; ++b) {
+    const int j0 = b * NB, nbk = std::min(NB, k - j0), L = rows - j0;
+    if (b > 0) cudaStreamWaitEvent(S.st, S.ev_pan, 0);  // panel b was factored on s2
+    F.b.push_back(Blk<FT>{V_of(b), L, L, nbk, T_of(b), j0});
+    const int c1 = j0 + nbk;
+    if (b + 1 < np) {
+      const int nbn = std::min(NB, k - c1);
+      if ((e = qr_update<FT>(M, ld, j0, L, nbk, c1, nbn, V_of(b), T_of(b), W, W2, work, wn, S.st))) return e;
+      cudaEventRecord(S.ev_upd, S.st);
+      cudaStreamWaitEvent(S.s2, S.ev_upd, 0);
+      if ((e = panel_factor<FT>(M, ld, c1, c1, rows - c1, nbn, false, taus + c1, V_of(b + 1), rows - c1,
+                                T_of(b + 1), 0, S.s2)))
+        return e;
+      cudaEventRecord(S.ev_pan, S.s2);
+      if ((e = qr_update<FT>(M, ld, j0, L, nbk, c1 + nbn, cend - c1 - nbn, V_of(b), T_of(b), W, W2, work,
+                             wn, S.st)))
+        return e;
+    } else {
+      if ((e = qr_update<FT>(M, ld, j0, L, nbk, c1, cend - c1, V_of(b), T_of(b), W, W2, work, wn, S.st)))
+        return e;
+    }
   }
   return cudaSuccess;
+}
+
+// rows [r0, r0+nr) of M[:, cb : cb+L] := (...) P = (...) - ((...) V) T V^H
+template <class FT>
+static cudaError_t rq_update(FT* M, int64_t ld, int r0, int nr, int cb, int L, int nbk, const FT* V,
+                             const FT* Tb, FT* W, FT* W2, FT* work, size_t wn, cudaStream_t st) {
+  if (nr <= 0) return cudaSuccess;
+  cudaError_t e;
+  FT* Ma = M + r0 + int64_t(cb) * ld;
+  if ((e = gemm<FT>(false, false, nr, nbk, L, 1.0, Ma, ld, V, L, 0.0, W, nr, work, wn, st))) return e;
+  if ((e = gemm<FT>(false, false, nr, nbk, nbk, 1.0, W, nr, Tb, NB, 0.0, W2, nr, nullptr, 0, st))) return e;
+  return gemm<FT>(false, true, nr, L, nbk, -1.0, W2, nr, V, L, 1.0, Ma, ld, nullptr, 0, st);
 }
 
 // RQ of the block rows [rb, rb+rr) x columns [cb, cb+cc) (rows bottom-up), applied
@@ -325,35 +373,46 @@ static cudaError_t qr_stage(FT* M, int64_t ld, int rows, int k, int cend, FT* Vb
 template <class FT>
 static cudaError_t rq_stage(FT* M, int64_t ld, int rb, int rr, int cb, int cc, FT* Vbuf, FT* Tbuf,
                             FT* taus, FT* W, FT* W2, FT* work, size_t wn, Fac<FT>& F,
-                            cudaStream_t st) {
+                            const Streams& S) {
   cudaError_t e;
   const int kk = std::min(rr, cc);
-  size_t voff = 0;
-  for (int r1 = kk, b = 0; r1 > 0; r1 -= NB, ++b) {
-    const int nbk = std::min(NB, r1);
-    // reflector j (0..kk-1): row rb + rr - kk + j, pivot column cb + cc - kk + j
-    const int jtop = r1 - 1;
-    const int64_t row_first = rb + rr - kk + jtop;
-    const int64_t pcmax = cb + cc - kk + jtop;
-    const int L = int(pcmax - cb + 1);
-    FT* V = Vbuf + voff;
-    FT* Tb = Tbuf + size_t(b) * NB * NB;
-    voff += size_t(L) * NB;
-    if ((e = panel_factor<FT>(M, ld, row_first, pcmax, L, nbk, true, taus + size_t(b) * NB, V, L, Tb,
-                              cb, st)))
-      return e;
-    F.b.push_back(Blk<FT>{V, L, L, nbk, Tb, 0});
-    const int above = int(row_first - (nbk - 1));  // rows [0, above)
-    if (above <= 0) continue;
-    FT* Ma = M + int64_t(cb) * ld;
-    // M_above := M_above P = M_above - (M_above V) T V^H
-    if ((e = gemm<FT>(false, false, above, nbk, L, 1.0, Ma, ld, V, L, 0.0, W, above, work, wn, st)))
-      return e;
-    if ((e = gemm<FT>(false, false, above, nbk, nbk, 1.0, W, above, Tb, NB, 0.0, W2, above, nullptr, 0,
-                      st)))
-      return e;
-    if ((e = gemm<FT>(false, true, above, L, nbk, -1.0, W2, above, V, L, 1.0, Ma, ld, nullptr, 0, st)))
-      return e;
+  const int np = (kk + NB - 1) / NB;
+  if (np == 0) return cudaSuccess;
+  // panel b: reflectors j in [r1 - nbk, r1), r1 = kk - b NB; row of j = rb + rr - kk + j,
+  // pivot column = cb + cc - kk + j
+  auto r1_of = [&](int b) { return kk - b * NB; };
+  auto nbk_of = [&](int b) { return std::min(NB, r1_of(b)); };
+  auto row_first = [&](int b) { return int64_t(rb + rr - kk + r1_of(b) - 1); };
+  auto pcmax = [&](int b) { return int64_t(cb + cc - kk + r1_of(b) - 1); };
+  auto L_of = [&](int b) { return int(pcmax(b) - cb + 1); };
+  std::vector<size_t> voff(np + 1, 0);
+  for (int b = 0; b < np; ++b) voff[b + 1] = voff[b] + size_t(L_of(b)) * NB;
+  auto V_of = [&](int b) { return Vbuf + voff[b]; };
+  auto T_of = [&](int b) { return Tbuf + size_t(b) * NB * NB; };
+  auto factor = [&](int b, cudaStream_t s) {
+    return panel_factor<FT>(M, ld, row_first(b), pcmax(b), L_of(b), nbk_of(b), true,
+                            taus + size_t(b) * NB, V_of(b), L_of(b), T_of(b), cb, s);
+  };
+  if ((e = factor(0, S.st))) return e;
+  for (int b = 0; b < np; ++b) {
+    if (b > 0) cudaStreamWaitEvent(S.st, S.ev_pan, 0);
+    const int L = L_of(b), nbk = nbk_of(b);
+    F.b.push_back(Blk<FT>{V_of(b), L, L, nbk, T_of(b), 0});
+    const int above = int(row_first(b) - (nbk - 1));  // rows [0, above)
+    if (b + 1 < np) {
+      const int nbn = nbk_of(b + 1);
+      if ((e = rq_update<FT>(M, ld, above - nbn, nbn, cb, L, nbk, V_of(b), T_of(b), W, W2, work, wn, S.st)))
+        return e;
+      cudaEventRecord(S.ev_upd, S.st);
+      cudaStreamWaitEvent(S.s2, S.ev_upd, 0);
+      if ((e = factor(b + 1, S.s2))) return e;
+      cudaEventRecord(S.ev_pan, S.s2);
+      if ((e = rq_update<FT>(M, ld, 0, above - nbn, cb, L, nbk, V_of(b), T_of(b), W, W2, work, wn, S.st)))
+        return e;
+    } else {
+      if ((e = rq_update<FT>(M, ld, 0, above, cb, L, nbk, V_of(b), T_of(b), W, W2, work, wn, S.st)))
+        return e;
+    }
   }
   return cudaSuccess;
 }
@@ -378,7 +437,7 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
                                      size_t(nbz + nbq) * NB * NB + size_t(C + R) + 2 * size_t(R) * NB +
                                      wn + 8 * size_t(L)) +
                        sizeof(WT) * (size_t(R) * (6 + ntc) + size_t(C) * (5 + ntr)) +
-                       sizeof(CT) * (10 * size_t(L) + 32 * 64) + 64 * 1024 + 64 * 256;
+                       sizeof(CT) * (10 * size_t(L) + 32 * 256) + 64 * 1024 + 64 * 256;
   cudaError_t e = ar.init(bytes + bytes / 4 + (1 << 20), st);
   if (e) return MLSB_ERR_CUDA;
   FT* M = ar.take<FT>(size_t(R) * C);
@@ -406,7 +465,7 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   WT* gvec = ar.take<WT>(C);
   CT* cv[10];
   for (int i = 0; i < 10; ++i) cv[i] = ar.take<CT>(L);
-  CT* ypart = ar.take<CT>(32 * 64);
+  CT* ypart = ar.take<CT>(32 * 256);
   char* small = ar.take<char>(64 * 1024);
   if (!small) return MLSB_ERR_CUDA;
   unsigned long long* bits = reinterpret_cast<unsigned long long*>(small);  // [8]
@@ -489,13 +548,30 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   cudaEventRecord(ev[1], st);
 
   // ---------------------------------------------------------- GRQ / GQR
+  Streams SS;
+  SS.st = st;
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&SS.s2, cudaStreamNonBlocking, hi);
+    cudaEventCreateWithFlags(&SS.ev_upd, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&SS.ev_pan, cudaEventDisableTiming);
+  }
+  struct StreamsGuard {
+    Streams& s;
+    ~StreamsGuard() {
+      cudaStreamDestroy(s.s2);
+      cudaEventDestroy(s.ev_upd);
+      cudaEventDestroy(s.ev_pan);
+    }
+  } sguard{SS};
   Fac<FT> FZ, FQ;  // QR factor (Z for LSE, Q for GLS) / RQ factor (Q^H for LSE, Z^H for GLS)
   if (lse) {
-    if ((e = rq_stage<FT>(M, ld, m, p, 0, n, VQ, TQ, tauQ, W, W2, gw, wn, FQ, st))) return MLSB_ERR_CUDA;
-    if ((e = qr_stage<FT>(M, ld, m, kz, n, VZ, TZ, tauZ, W, W2, gw, wn, FZ, st))) return MLSB_ERR_CUDA;
+    if ((e = rq_stage<FT>(M, ld, m, p, 0, n, VQ, TQ, tauQ, W, W2, gw, wn, FQ, SS))) return MLSB_ERR_CUDA;
+    if ((e = qr_stage<FT>(M, ld, m, kz, n, VZ, TZ, tauZ, W, W2, gw, wn, FZ, SS))) return MLSB_ERR_CUDA;
   } else {
-    if ((e = qr_stage<FT>(M, ld, n, kz, m + p, VZ, TZ, tauZ, W, W2, gw, wn, FZ, st))) return MLSB_ERR_CUDA;
-    if ((e = rq_stage<FT>(M, ld, 0, n, m, p, VQ, TQ, tauQ, W, W2, gw, wn, FQ, st))) return MLSB_ERR_CUDA;
+    if ((e = qr_stage<FT>(M, ld, n, kz, m + p, VZ, TZ, tauZ, W, W2, gw, wn, FZ, SS))) return MLSB_ERR_CUDA;
+    if ((e = rq_stage<FT>(M, ld, 0, n, m, p, VQ, TQ, tauQ, W, W2, gw, wn, FQ, SS))) return MLSB_ERR_CUDA;
   }
   // zero pivots in the order of the reference's first failing trsv
   // (LSE: R at lse.hpp:53, then T11 at :60; GLS: T22 at gls.hpp:55, then R at :61)

@@ -36,6 +36,7 @@ struct PanelArgs {
   T* M;
   int64_t ld, r0, c0;
   int L, nb, rc;  // panel rows, reflectors, rows per CTA
+  int ncl;        // CTAs in the cluster
   bool rq;
   T* tau;
   T* V;
@@ -140,13 +141,23 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs<T> a) {
     if (tid < 2 * NB) {
       const int k = tid < NB ? tid : tid - NB;
       if (k < nb) {
+        T v[PCL];
+#pragma unroll
+        for (int c = 0; c < PCL; ++c) v[c] = c < a.ncl ? cl.map_shared_rank(part, c)[par * NV + tid] : zero<T>();
         T s = zero<T>();
-        for (int c = 0; c < PCL; ++c) s = s + cl.map_shared_rank(part, c)[par * NV + tid];
+#pragma unroll
+        for (int c = 0; c < PCL; ++c)
+          if (c < a.ncl) s = s + v[c];
         tot[tid] = s;
       }
     } else if (tid == 2 * NB) {
+      double v[PCL];
+#pragma unroll
+      for (int c = 0; c < PCL; ++c) v[c] = c < a.ncl ? cl.map_shared_rank(partd, c)[par] : 0.0;
       double s = 0.0;
-      for (int c = 0; c < PCL; ++c) s += cl.map_shared_rank(partd, c)[par];
+#pragma unroll
+      for (int c = 0; c < PCL; ++c)
+        if (c < a.ncl) s += v[c];
       totd[0] = s;
     }
     __syncthreads();
@@ -165,14 +176,16 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs<T> a) {
       if (k == q) taus[q] = tau;
     }
     __syncthreads();
-    // ---- apply H^H to my rows of columns k > q; finish column q
+    // ---- apply H^H to my rows of columns k > q (warp per column, lanes over rows)
     const bool has_tau = !(tau == zero<T>());
-    for (int e = tid; e < (re - rb) * nb; e += PNT) {
-      const int r = rb + e % (re - rb), k = e / (re - rb);
-      T* pe = P + (r - rb) + k * ldp;
-      if (k > q && has_tau) {
-        if (r == q) *pe = *pe - coef[k];
-        else if (r > q) *pe = *pe - coef[k] * (inv * xq[r - rb]);
+    if (has_tau) {
+      for (int k = q + 1 + w; k < nb; k += PNW) {
+        const T ck = coef[k];
+        T* pk = P + k * ldp;
+        for (int r = max(rb, q) + l; r < re; r += 32) {
+          if (r == q) pk[r - rb] = pk[r - rb] - ck;
+          else pk[r - rb] = pk[r - rb] - ck * (inv * xq[r - rb]);
+        }
       }
     }
     __syncthreads();
@@ -238,6 +251,9 @@ cudaError_t panel_factor(T* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb
   a.c0 = c0;
   a.L = L;
   a.nb = nb;
+  // 16 CTAs (B200's non-portable maximum): the per-step work is the rows each
+  // CTA owns, measured cheaper than the extra cluster-barrier cost
+  a.ncl = PCL;
   a.rc = (L + PCL - 1) / PCL;
   a.rq = rq;
   a.tau = tau;
@@ -257,13 +273,13 @@ cudaError_t panel_factor(T* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb
   }
   if (sm > 227 * 1024) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(PCL);
+  cfg.gridDim = dim3(a.ncl);
   cfg.blockDim = dim3(PNT);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = PCL;
+  attr[0].val.clusterDim.x = a.ncl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;

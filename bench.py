@@ -136,6 +136,19 @@ def cpu_reference(A, B, b, d, seconds, maxit=40, prec=("s", "s", "d")):
     return k / dt, threads, kind, k, dt
 
 
+def measured_traffic(batch):
+    """DRAM bytes (read + write) per launch of the tile solver from the committed
+    `ncu --set full` capture (profiles/c4_ncu_summary.json), scaled to `batch`
+    problems; None when no capture is committed."""
+    path = os.path.join(ROOT, "profiles", "c4_ncu_summary.json")
+    try:
+        with open(path) as fh:
+            s = json.load(fh)
+        return s["dram_bytes_per_problem"] * batch
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def emit(obj):
     print(json.dumps(obj), flush=True)
 
@@ -157,9 +170,11 @@ def run_reference(args, rank, world):
         return
     from paper_2406_16499_b200 import generate as G
 
-    # bounded sample of the C4 workload, generated on the CPU (numpy)
+    # bounded sample of the C4 workload, generated on the host (same generator,
+    # CPU RNG stream)
     S = 4096
-    A, B, b, d, _ = G.lse_batch_numpy(S, M, N, P, seed=1000)
+    A, B, b, d, _ = G.lse_batch_torch(S, M, N, P, seed=1000, device="cpu")
+    A, B, b, d = A.numpy(), B.numpy(), b.numpy(), d.numpy()
     vals = []
     info = None
     for step in range(args.warmup + args.steps):
@@ -253,8 +268,8 @@ def run_ours(args, rank, world, local_rank):
         "config": config_c4(batch, world),
         "roofline": {"bound": "hbm", "achieved": alg_bytes / kern_s / 1e9,
                      "peak": hbm, "unit": "GB/s", "frac": alg_bytes / kern_s / 1e9 / hbm,
-                     "traffic": None,
-                     "kernel": "tile_solve_kernel<LSE,float,float,false>",
+                     "traffic": measured_traffic(batch),
+                     "kernel": "lse_reg_kernel<float>",
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
         "roofline_fp32": {"bound": "fp32_simt", "achieved": alg_flops / kern_s / 1e12,
@@ -314,19 +329,23 @@ def run_ours(args, rank, world, local_rank):
         result["e2e"] = {"value": world * batch * ke / dt, "unit": "solves/s",
                          "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                          "steps": ke, "api": "mlsb_mplse_batched (C ABI), pinned host buffers"}
-        del hA, hB
 
     # ---- CPU baseline: the reference on this host, bounded sample, rank 0, N=1
+    # (the full batch when it fits in ~cpu_seconds)
     if rank == 0 and world == 1 and not args.no_cpu:
-        S = 4096
-        An = A[:S].cpu().numpy()
-        Bn = B[:S].cpu().numpy()
-        bn = b[:S].cpu().numpy()
-        dn = d[:S].cpu().numpy()
+        if args.no_e2e:
+            S = min(batch, 16384)
+            An, Bn = A[:S].cpu().numpy(), B[:S].cpu().numpy()
+            bn, dn = b[:S].cpu().numpy(), d[:S].cpu().numpy()
+        else:  # the pinned host copies (same problems, no second 19 GB copy)
+            An, Bn, bn, dn = hA.numpy(), hB.numpy(), hb.numpy(), hd.numpy()
         v, cores, kind, k, dt = cpu_reference(An, Bn, bn, dn, args.cpu_seconds)
         result["cpu_baseline"] = {"value": v, "unit": "solves/s", "cores": cores, "kind": kind,
-                                  "sample": f"first {k} of the same C4 problems "
+                                  "sample": f"first {k} of the same {batch} C4 problems "
                                             f"({dt:.1f} s, std::thread pool over {cores} threads)"}
+        del An, Bn
+    if not args.no_e2e:
+        del hA, hB
     if rank == 0:
         emit(result)
 

@@ -410,7 +410,7 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
     unsigned long long h[64];
     cudaMemcpy(h, a.stamps, sizeof(h), cudaMemcpyDeviceToHost);
     fprintf(stderr, "MLSB_STAMPS(us from start):");
-    for (int i = 1; i < 16; ++i)
+    for (int i = 1; i < 32; ++i)
       if (h[i]) fprintf(stderr, " [%d] %.1f", i, (h[i] - h[0]) * 1e-3);
     fprintf(stderr, "\n");
 

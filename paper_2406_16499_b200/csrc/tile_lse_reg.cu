@@ -43,7 +43,7 @@ __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15)
 
 struct Layout {
   int R, C, ld, kz, nbz, nbq;
-  size_t oM, oTau1, oTau2, oTZ, oTQ, oU, oRinit, oRout, oSw, oCout, oSu, oWork, oYb, oRed,
+  size_t oM, oTau1, oTau2, oTZ, oTQ, oU, oRinit, oRout, oSw, oCout, oSu, oWork, oRed,
       oScal, oRinv, total;
 };
 
@@ -59,11 +59,11 @@ __host__ __device__ inline Layout make_layout(int64_t m, int64_t n, int64_t p, i
   L.oM = o;     o = al16(o + size_t(L.ld) * L.C * 4);
   L.oTau1 = o;  o = al16(o + size_t(CMAX) * 4);
   L.oTau2 = o;  o = al16(o + size_t(RMAX) * 4);
-  L.oTZ = o;    o = al16(o + size_t(L.nbz) * 1024 * 4);
-  L.oTQ = o;    o = al16(o + size_t(L.nbq) * 1024 * 4);
+  L.oTZ = o;    o = al16(o + size_t(L.nbz) * 32 * 33 * 4);
+  L.oTQ = o;    o = al16(o + size_t(L.nbq) * 32 * 33 * 4);
   // union: factorization scratch (fp32 partials + w + 2 reflector buffers) |
   //        refinement scratch (fp64 row partials CG x RMAX + col partials 2 x CMAX)
-  const size_t fac = size_t(NW) * RMAX * 4 + RMAX * 4 + 2 * RMAX * 4;
+  const size_t fac = size_t(NW) * RMAX * 4 + RMAX * 4 + 4 * RMAX * 4;  // ... + NVB reflector buffers
   const size_t ref = size_t(CG) * RMAX * 8 + 2 * CMAX * 8;
   L.oU = o;     o = al16(o + (fac > ref ? fac : ref));
   L.oRinit = o; o = al16(o + size_t(RMAX) * 8);
@@ -72,7 +72,6 @@ __host__ __device__ inline Layout make_layout(int64_t m, int64_t n, int64_t p, i
   L.oCout = o;  o = al16(o + size_t(CMAX) * 8);
   L.oSu = o;    o = al16(o + size_t(CMAX) * 8);
   L.oWork = o;  o = al16(o + size_t(NWORK) * RMAX * csz);
-  L.oYb = o;    o = al16(o + size_t(NW) * 32 * csz);
   L.oRed = o;   o = al16(o + size_t(NW) * 8 * 8);
   L.oScal = o;  o = al16(o + 64 * 8);
   L.oRinv = o;  o = al16(o + size_t(2) * CMAX * csz + size_t(2) * CMAX * 4);
@@ -81,7 +80,7 @@ __host__ __device__ inline Layout make_layout(int64_t m, int64_t n, int64_t p, i
 }
 
 enum Slot { S_SA = 0, S_SB, S_CB, S_CD, S_NB, S_ND, S_NA, S_NBF, S_SIG, S_BETA, S_ALPHA,
-            S_RED0 = 16, S_FLAG = 40 };
+            S_RED0 = 16, S_FLAG = 40, S_MBAR = 48 };
 
 // ---------------------------------------------------------------- helpers
 // 8 partial sums per lane -> lane-complete sums (8-way transposed butterfly:
@@ -123,119 +122,134 @@ __device__ __forceinline__ void reduce8(float (&d)[8], int l) {
   for (int i = 0; i < 8; ++i) d[i] = x.d[i];
 }
 
-// ------------------------------------------------------- WY block applies
-// QR factor (Z): block of kb reflectors j0..j0+kb-1 stored in columns of M
-// (v_j = e_j + M[j+1:rend, j]).  x := (I - V T' V^T) x, T' = T or T^T.
+// ------------------------------------------- multi-warp WY block applies
+// T blocks (32 x 32, forward xLARFT) use a padded column stride so that both
+// row and column walks by a warp are bank-conflict free.
+constexpr int TLD = 33, TSZ = 32 * TLD;
+
+// A warp group: ngw warps with named barrier `bar` (0 = the whole CTA).
+struct Grp {
+  int gw, ngw, l, bar;
+  __device__ __forceinline__ void sync() const {
+    if (bar == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * ngw) : "memory");
+  }
+};
+
+// Transposed butterfly: lane l returns sum over the warp's lanes of v[l] * xv
+// (16 + 8 + 4 + 2 + 1 exchanges, fixed order).
 template <class CT>
-__device__ void zblk(const float* M, int ld, int j0, int kb, int rend, const float* Tb, bool tr,
-                     CT* x, CT* yb, int l) {
-  CT y = CT(0);
-  if (l < kb) {
-    const int jq = j0 + l;
-    const float* col = M + size_t(jq) * ld;
-    CT y0 = x[jq], y1 = CT(0), y2 = CT(0), y3 = CT(0);
-    int r = jq + 1;
-    for (; r + 3 < rend; r += 4) {
-      y0 += CT(col[r]) * x[r];
-      y1 += CT(col[r + 1]) * x[r + 1];
-      y2 += CT(col[r + 2]) * x[r + 2];
-      y3 += CT(col[r + 3]) * x[r + 3];
-    }
-    for (; r < rend; ++r) y0 += CT(col[r]) * x[r];
-    y = (y0 + y1) + (y2 + y3);
+__device__ __forceinline__ CT tsum32(const float (&v)[32], CT xv, int l) {
+  CT d[16];
+  const bool b4 = l & 16, b3 = l & 8, b2 = l & 4, b1 = l & 2, b0 = l & 1;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const CT lo = CT(v[i]) * xv, hi = CT(v[i + 16]) * xv;
+    const CT send = b4 ? lo : hi, keep = b4 ? hi : lo;
+    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
   }
-  yb[l] = y;
-  __syncwarp();
-  CT z = CT(0);
-  if (l < kb) {
-    if (!tr)
-      for (int k = l; k < kb; ++k) z += CT(Tb[l + 32 * k]) * yb[k];
-    else
-      for (int k = 0; k <= l; ++k) z += CT(Tb[k + 32 * l]) * yb[k];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const CT send = b3 ? d[i] : d[i + 8], keep = b3 ? d[i + 8] : d[i];
+    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
   }
-  __syncwarp();
-  yb[l] = z;
-  __syncwarp();
-  for (int r = j0 + l; r < rend; r += 32) {
-    const int qmax = (r - j0 + 1) < kb ? (r - j0 + 1) : kb;  // reflectors q with j0+q <= r
-    CT acc = CT(0);
-    for (int q = 0; q < qmax; ++q) {
-      const int jq = j0 + q;
-      const CT vq = (r == jq) ? CT(1) : CT(M[r + size_t(jq) * ld]);
-      acc += vq * yb[q];
-    }
-    x[r] -= acc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const CT send = b2 ? d[i] : d[i + 4], keep = b2 ? d[i + 4] : d[i];
+    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
   }
-  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const CT send = b1 ? d[i] : d[i + 2], keep = b1 ? d[i + 2] : d[i];
+    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  const CT send = b0 ? d[0] : d[1], keep = b0 ? d[1] : d[0];
+  return keep + __shfl_xor_sync(0xffffffffu, send, 1);
 }
 
-// Z x (herm = false: last block first, T) or Z^T x (first block first, T^T)
+// One block of kb <= 32 reflectors applied to the entries [i0, i1) of x
+// (i1 - i0 <= 32 ngw, one entry per thread): x := x - V T' (V^T x).  The
+// thread's row of V stays in registers between the two products; V^T x is a
+// transposed warp reduction plus a fixed-order sum over the group's warps
+// (`part`, double-buffered by the caller, so one barrier per block).
+template <class CT, class VF>
+__device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, const float* Tb,
+                                         bool tr, CT* x, CT* part, const Grp& g) {
+  const int l = g.l, i = i0 + 32 * g.gw + l;
+  const bool act = i < i1;
+  float v[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) v[q] = (act && q < kb) ? vf(i, q) : 0.f;
+  const CT xi = act ? x[i] : CT(0);
+  part[32 * g.gw + l] = tsum32(v, xi, l);
+  g.sync();
+  CT y = CT(0);
+  for (int w2 = 0; w2 < g.ngw; ++w2) y += part[32 * w2 + l];
+  // z = T' y, lane l -> z_l
+  CT z0 = CT(0), z1 = CT(0);
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const CT yk = __shfl_sync(0xffffffffu, y, k);
+    const bool use = k < kb && (tr ? k <= l : k >= l);
+    const float t = use ? (tr ? Tb[k + TLD * l] : Tb[l + TLD * k]) : 0.f;
+    if (k & 1) z1 += CT(t) * yk;
+    else z0 += CT(t) * yk;
+  }
+  const CT z = l < kb ? z0 + z1 : CT(0);
+  CT a0 = CT(0), a1 = CT(0);
+#pragma unroll
+  for (int q = 0; q < 32; q += 2) {
+    a0 += CT(v[q]) * __shfl_sync(0xffffffffu, z, q);
+    a1 += CT(v[q + 1]) * __shfl_sync(0xffffffffu, z, q + 1);
+  }
+  if (act) x[i] = xi - (a0 + a1);
+}
+
+// QR (Z) reflectors: v_q = e_{j0+q} + M[j0+q+1 : rend, j0+q]; entry index = row
+struct ZV {
+  const float* M;
+  int ld, j0;
+  __device__ __forceinline__ float operator()(int r, int q) const {
+    const int d = r - j0;
+    return d > q ? M[r + size_t(j0 + q) * ld] : (d == q ? 1.f : 0.f);
+  }
+};
+// RQ (Q) reflectors in rows rtop + j: entries at columns c < ptop + j, unit at
+// c = ptop + j; entry index = column
+struct QV {
+  const float* M;
+  int ld, row0, pc0;  // row0 = rtop + j0, pc0 = ptop + j0
+  __device__ __forceinline__ float operator()(int c, int q) const {
+    const int pc = pc0 + q;
+    return c < pc ? M[(row0 + q) + size_t(c) * ld] : (c == pc ? 1.f : 0.f);
+  }
+};
+
+// Z x (herm = false: last block first, T) or Z^T x (first block first, T^T);
+// group of >= ceil(rend / 32) warps.  Two applies by the same group must be
+// separated by a barrier (the part buffers restart at 0).
 template <class CT>
-__device__ void z_apply(const float* M, int ld, int k, int rend, const float* TZ, bool herm, CT* x,
-                        CT* yb, int l) {
+__device__ void z_apply_mw(const float* M, int ld, int k, int rend, const float* TZ, bool herm,
+                           CT* x, CT* part, const Grp& g) {
   const int nb = (k + 31) / 32;
   for (int s = 0; s < nb; ++s) {
     const int b = herm ? s : nb - 1 - s;
     const int j0 = 32 * b, kb = (k - j0) < 32 ? (k - j0) : 32;
-    zblk(M, ld, j0, kb, rend, TZ + b * 1024, herm, x, yb, l);
+    wy_block(ZV{M, ld, j0}, j0, rend, kb, TZ + b * TSZ, herm, x, part + (s & 1) * 32 * g.ngw, g);
   }
 }
 
-// RQ factor (Q): reflector j in row rtop+j, entries at columns c < ptop+j,
-// unit at c = ptop+j; block of kb reflectors from j0.
+// Q x / Q^T x over the first dim entries; group of >= ceil(dim / 32) warps
 template <class CT>
-__device__ void qblk(const float* M, int ld, int rtop, int ptop, int j0, int kb, int dim,
-                     const float* Tb, bool tr, CT* x, CT* yb, int l) {
-  CT y = CT(0);
-  if (l < kb) {
-    const int jq = j0 + l, pc = ptop + jq;
-    const float* row = M + (rtop + jq);
-    CT y0 = x[pc], y1 = CT(0), y2 = CT(0), y3 = CT(0);
-    int c = 0;
-    for (; c + 3 < pc; c += 4) {
-      y0 += CT(row[size_t(c) * ld]) * x[c];
-      y1 += CT(row[size_t(c + 1) * ld]) * x[c + 1];
-      y2 += CT(row[size_t(c + 2) * ld]) * x[c + 2];
-      y3 += CT(row[size_t(c + 3) * ld]) * x[c + 3];
-    }
-    for (; c < pc; ++c) y0 += CT(row[size_t(c) * ld]) * x[c];
-    y = (y0 + y1) + (y2 + y3);
-  }
-  yb[l] = y;
-  __syncwarp();
-  CT z = CT(0);
-  if (l < kb) {
-    if (!tr)
-      for (int k = l; k < kb; ++k) z += CT(Tb[l + 32 * k]) * yb[k];
-    else
-      for (int k = 0; k <= l; ++k) z += CT(Tb[k + 32 * l]) * yb[k];
-  }
-  __syncwarp();
-  yb[l] = z;
-  __syncwarp();
-  const int cmax = ptop + j0 + kb;  // columns touched by the block
-  for (int c = l; c < cmax && c < dim; c += 32) {
-    CT acc = CT(0);
-    for (int q = 0; q < kb; ++q) {
-      const int pc = ptop + j0 + q;
-      if (c <= pc) {
-        const CT vq = (c == pc) ? CT(1) : CT(M[(rtop + j0 + q) + size_t(c) * ld]);
-        acc += vq * yb[q];
-      }
-    }
-    x[c] -= acc;
-  }
-  __syncwarp();
-}
-
-template <class CT>
-__device__ void q_apply(const float* M, int ld, int kq, int rtop, int ptop, int dim,
-                        const float* TQ, bool herm, CT* x, CT* yb, int l) {
+__device__ void q_apply_mw(const float* M, int ld, int kq, int rtop, int ptop, int dim,
+                           const float* TQ, bool herm, CT* x, CT* part, const Grp& g) {
   const int nb = (kq + 31) / 32;
   for (int s = 0; s < nb; ++s) {
     const int b = herm ? s : nb - 1 - s;
     const int j0 = 32 * b, kb = (kq - j0) < 32 ? (kq - j0) : 32;
-    qblk(M, ld, rtop, ptop, j0, kb, dim, TQ + b * 1024, herm, x, yb, l);
+    const int cmax = (ptop + j0 + kb) < dim ? (ptop + j0 + kb) : dim;
+    wy_block(QV{M, ld, rtop + j0, ptop + j0}, 0, cmax, kb, TQ + b * TSZ, herm, x,
+             part + (s & 1) * 32 * g.ngw, g);
   }
 }
 
@@ -363,7 +377,7 @@ __device__ void gemv_cols(const float* M, int ld, int r0, int rows, int c0, int 
 }
 
 // T of a forward block (xLARFT): T[q][q] = tau_q; T[0:q,q] = -tau_q T[0:q,0:q] G[0:q,q].
-// G (upper Gram, column-major 32x32) is overwritten by T.  One warp; lane l keeps
+// G (upper Gram, column-major 32x32, column stride TLD) is overwritten by T.  One warp; lane l keeps
 // row l of T in registers so the recurrence only streams G.
 __device__ void build_T(float* G, const float* tau, int kb, int l) {
   float Tr[32];
@@ -374,7 +388,7 @@ __device__ void build_T(float* G, const float* tau, int kb, int l) {
     if (q < kb) {
       float t = 0.f;
 #pragma unroll
-      for (int k = 0; k < q; ++k) t = fmaf(Tr[k], G[k + 32 * q], t);
+      for (int k = 0; k < q; ++k) t = fmaf(Tr[k], G[k + TLD * q], t);
       const float tq = tau[q];
       Tr[q] = (l < q) ? -tq * t : (l == q ? tq : 0.f);
     }
@@ -383,7 +397,7 @@ __device__ void build_T(float* G, const float* tau, int kb, int l) {
   if (l < kb)
 #pragma unroll
     for (int q = 0; q < 32; ++q)
-      if (q < kb) G[l + 32 * q] = Tr[q];
+      if (q < kb) G[l + TLD * q] = Tr[q];
   __syncwarp();
 }
 
@@ -547,27 +561,74 @@ __device__ __forceinline__ void reduce16(float (&d)[16], int l) {
   for (int i = 0; i < 16; ++i) d[i] = x.d[i];
 }
 
+// Reflector hand-off between warps: a ring of NVB reflector buffers guarded by
+// mbarriers instead of a CTA barrier per reflector.  full[b] (32 arrivals:
+// the owner warp's lanes, after writing v and tau) publishes a reflector;
+// empty[b] (NW arrivals, one per warp after its last read of v) releases
+// the buffer for the reflector NVB steps later.  A warp waits only for the
+// reflector it applies next, so no warp waits for the slowest warp of the
+// previous step, and the owner of the next column (row) updates and
+// generates it before doing anything else (the serial chain of the
+// factorization).
+constexpr int NVB = 4;
+
+// RQ owner path: apply reflector (vv, tj) to the owner's row slot TO, then
+// generate the next reflector (index jn, pivot pc, sequence number kn) from it.
+template <int TO>
+__device__ __forceinline__ void rq_crit(float (&br)[BT][BS], const float (&vv)[BS], float tj, int jn,
+                                        int pc, int C, int l, float* vbuf, float* tau2,
+                                        uint64_t* full, uint64_t* empty, int kn) {
+  float dc = 0.f;
+#pragma unroll
+  for (int s = 0; s < BS; ++s) dc = fmaf(br[TO][s], vv[s], dc);
+  dc = warp_sum(dc);
+  if (tj != 0.f)
+#pragma unroll
+    for (int s = 0; s < BS; ++s) br[TO][s] = fmaf(-(tj * vv[s]), dc, br[TO][s]);
+  const int b = kn % NVB;
+  if (kn >= NVB) mbar_wait(empty + b, ((kn / NVB) - 1) & 1);
+  gen_row<TO>(br, jn, pc, C, l, vbuf + b * CMAX, tau2);
+  __syncwarp();
+  mbar_arrive(full + b);
+}
+
 // RQ steps for the reflector rows of row slot TO (rows 16 TO + 15 ... 16 TO),
-// bottom-up.  Reflector j (row m+j, pivot n-p+j) is applied from the right to
-// every row above it; the Gram entries v_j^T v_k of already processed rows k
-// of the same block of 32 come out of the same reduction (v_j vanishes past
-// its pivot, where v_k still holds explicit entries).
+// bottom-up.  Reflector j (row m+j, pivot n-p+j, sequence number p-1-j) is
+// applied from the right to every row above it; the Gram entries v_j^T v_k of
+// already processed rows k of the same block of 32 come out of the same
+// reduction (v_j vanishes past its pivot, where v_k still holds explicit
+// entries).
 template <int TO>
 __device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p, int C, int w,
-                                        int l, float* vbuf, float* tau2, float* TQ) {
+                                        int l, float* vbuf, float* tau2, float* TQ, uint64_t* full,
+                                        uint64_t* empty) {
+  if (NW * TO + NW - 1 < m || NW * TO >= m + p) return;  // no reflector rows in this slot
 #pragma unroll 1
   for (int wo = NW - 1; wo >= 0; --wo) {
     const int row = NW * TO + wo, j = row - m;
     if (j < 0 || j >= p) continue;
-    if (j == p - 1 && w == wo) gen_row<TO>(br, j, n - p + j, C, l, vbuf + (j & 1) * CMAX, tau2);
-    __syncthreads();
+    const int k = p - 1 - j, b = k % NVB;
+    if (k == 0 && w == wo) {
+      gen_row<TO>(br, j, n - p + j, C, l, vbuf, tau2);
+      __syncwarp();
+      mbar_arrive(full);
+    }
+    mbar_wait(full + b, (k / NVB) & 1);
     const float tj = tau2[j];
-    const float* v = vbuf + (j & 1) * CMAX;
+    const float* v = vbuf + b * CMAX;
     float vv[BS];
 #pragma unroll
     for (int s = 0; s < BS; ++s) {
       const int c = l + 32 * s;
       vv[s] = c < C ? v[c] : 0.f;
+    }
+    const bool own = j >= 1 && w == ((row - 1) & (NW - 1));
+    if (own) {
+      if (wo > 0)
+        rq_crit<TO>(br, vv, tj, j - 1, n - p + j - 1, C, l, vbuf, tau2, full, empty, k + 1);
+      else
+        rq_crit<(TO > 0 ? TO - 1 : 0)>(br, vv, tj, j - 1, n - p + j - 1, C, l, vbuf, tau2, full,
+                                       empty, k + 1);
     }
     float d[16], e0 = 0.f, e1 = 0.f;
 #pragma unroll
@@ -581,6 +642,8 @@ __device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p
       e0 = fmaf(br[16][s], vv[s], e0);
       e1 = fmaf(br[17][s], vv[s], e1);
     }
+    __syncwarp();
+    if (l == 0) mbar_arrive(empty + b);
     reduce16(d, l);
     e0 = warp_sum(e0);
     e1 = warp_sum(e1);
@@ -590,46 +653,72 @@ __device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p
       const int i = w + NW * t;
       const float dt = t < 16 ? d[t < 16 ? t : 0] : (t == 16 ? e0 : e1);
       if (i < row) {
-        if (tj != 0.f)
+        if (tj != 0.f && !(own && i == row - 1))
 #pragma unroll
           for (int s = 0; s < BS; ++s) br[t][s] = fmaf(-(tj * vv[s]), dt, br[t][s]);
       } else if (i > row && i < m + p) {
-        const int k = i - m;
-        if (l == 0 && (k & ~31) == jb) TQ[(jb >> 5) * 1024 + (j - jb) + 32 * (k - jb)] = dt;
-      }
-    }
-    if (j >= 1) {
-      const int row1 = row - 1;
-      if (w == (row1 & (NW - 1))) {
-        if (wo > 0) gen_row<TO>(br, j - 1, n - p + j - 1, C, l, vbuf + ((j - 1) & 1) * CMAX, tau2);
-        else gen_row<(TO > 0 ? TO - 1 : 0)>(br, j - 1, n - p + j - 1, C, l,
-                                           vbuf + ((j - 1) & 1) * CMAX, tau2);
+        const int kk = i - m;
+        if (l == 0 && (kk & ~31) == jb) TQ[(jb >> 5) * TSZ + (j - jb) + TLD * (kk - jb)] = dt;
       }
     }
   }
 }
 
+// QR owner path: apply reflector j (vr, tj) to column j1 = j + 1 in slot S1,
+// then generate reflector j1 from it.
+template <int S1, int T0>
+__device__ __forceinline__ void qr_crit(float (&ar)[RT][CS], const float (&vr)[RT], float tj, int j1,
+                                        int m, int l, float* vbuf, float* tau1, uint64_t* full,
+                                        uint64_t* empty) {
+  float dc = 0.f;
+#pragma unroll
+  for (int t = T0; t < RT; ++t)
+    if (32 * t < m) dc = fmaf(ar[t][S1], vr[t], dc);
+  dc = warp_sum(dc);
+  if (tj != 0.f) {
+    const float sc = tj * dc;
+#pragma unroll
+    for (int t = T0; t < RT; ++t)
+      if (32 * t < m) ar[t][S1] = fmaf(-sc, vr[t], ar[t][S1]);
+  }
+  const int b = j1 % NVB;
+  if (j1 >= NVB) mbar_wait(empty + b, ((j1 / NVB) - 1) & 1);
+  gen_col<S1>(ar, j1, m, l, vbuf + b * RMAX, tau1);
+  __syncwarp();
+  mbar_arrive(full + b);
+}
+
 // QR steps for the columns of slot SC (j = 16 SC + jw).  Column c is owned by
-// warp c % 16; the owner of column j+1 updates it first and generates
-// reflector j+1 before the next barrier (look-ahead).  Within slot SC the
-// live part of the register tile is static: rows >= j live in row slots
-// t >= SC/2, and columns >= the Gram block start live in slots s >= SC & ~1,
-// so finished rows/columns cost no instructions.
+// warp c % 16.  Within slot SC the live part of the register tile is static:
+// rows >= j live in row slots t >= SC/2, and columns >= the Gram block start
+// live in slots s >= SC & ~1, so finished rows/columns cost no instructions.
 template <int SC>
 __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int kz, int w, int l,
-                                        float* vbuf, float* tau1, float* TZ) {
+                                        float* vbuf, float* tau1, float* TZ, uint64_t* full,
+                                        uint64_t* empty) {
   constexpr int T0 = SC / 2, S0 = SC & ~1;
 #pragma unroll 1
   for (int jw = 0; jw < NW; ++jw) {
     const int j = NW * SC + jw;
     if (j >= kz) return;
-    if (SC == 0 && j == 0 && w == 0) gen_col<0>(ar, 0, m, l, vbuf, tau1);
-    __syncthreads();
+    if (SC == 0 && j == 0 && w == 0) {
+      gen_col<0>(ar, 0, m, l, vbuf, tau1);
+      __syncwarp();
+      mbar_arrive(full);
+    }
+    const int b = j % NVB;
+    mbar_wait(full + b, (j / NVB) & 1);
     const float tj = tau1[j];
-    const float* v = vbuf + (j & 1) * RMAX;
+    const float* v = vbuf + b * RMAX;
     float vr[RT];
 #pragma unroll
-    for (int t = T0; t < RT; ++t) vr[t] = v[l + 32 * t];
+    for (int t = 0; t < RT; ++t) vr[t] = t >= T0 ? v[l + 32 * t] : 0.f;
+    const int j1 = j + 1;
+    const bool own = j1 < kz && w == (j1 & (NW - 1));
+    if (own) {
+      if (jw < NW - 1) qr_crit<SC, T0>(ar, vr, tj, j1, m, l, vbuf, tau1, full, empty);
+      else qr_crit<(SC + 1 < CS ? SC + 1 : SC), T0>(ar, vr, tj, j1, m, l, vbuf, tau1, full, empty);
+    }
     const int bstart = j & ~31;
     float d[CS];
 #pragma unroll
@@ -640,32 +729,17 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
 #pragma unroll
       for (int s = S0; s < CS; ++s) d[s] = fmaf(ar[t][s], vr[t], d[s]);
     }
+    __syncwarp();
+    if (l == 0) mbar_arrive(empty + b);
     reduce8(d, l);
-    // slots SC and SC+1 (where column j+1 lives) first
-#pragma unroll
-    for (int s = SC; s < CS && s <= SC + 1; ++s) {
-      const int c = w + NW * s;
-      if (c > j && c < C && tj != 0.f) {
-        const float sc = tj * d[s];
-#pragma unroll
-        for (int t = T0; t < RT; ++t)
-          if (32 * t < m) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
-      }
-    }
-    const int j1 = j + 1;
-    if (j1 < kz && w == (j1 & (NW - 1))) {
-      if (jw < NW - 1) gen_col<SC>(ar, j1, m, l, vbuf + (j1 & 1) * RMAX, tau1);
-      else gen_col<(SC + 1 < CS ? SC + 1 : SC)>(ar, j1, m, l, vbuf + (j1 & 1) * RMAX, tau1);
-    }
 #pragma unroll
     for (int s = S0; s < CS; ++s) {
       const int c = w + NW * s;
       if (c >= bstart && c < j) {
-        if (l == 0) TZ[(bstart >> 5) * 1024 + (c - bstart) + 32 * (j - bstart)] = d[s];
+        if (l == 0) TZ[(bstart >> 5) * TSZ + (c - bstart) + TLD * (j - bstart)] = d[s];
         continue;
       }
-      if (s == SC || s == SC + 1) continue;
-      if (c > j && c < C && tj != 0.f) {
+      if (c > j && c < C && tj != 0.f && !(own && c == j1)) {
         const float sc = tj * d[s];
 #pragma unroll
         for (int t = T0; t < RT; ++t)
@@ -693,7 +767,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   float* TQ = reinterpret_cast<float*>(smem + Ly.oTQ);
   float* fpart = reinterpret_cast<float*>(smem + Ly.oU);           // [NW][RMAX]
   float* wbuf = fpart + NW * RMAX;                                  // [RMAX]
-  float* vbuf = wbuf + RMAX;                                        // [2][RMAX]
+  float* vbuf = wbuf + RMAX;                                        // [NVB][RMAX]
   double* dpart = reinterpret_cast<double*>(smem + Ly.oU);         // [CG][RMAX]
   double* cpart = dpart + CG * RMAX;                                // [2][CMAX]
   double* rinit = reinterpret_cast<double*>(smem + Ly.oRinit);
@@ -703,11 +777,14 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   double* su = reinterpret_cast<double*>(smem + Ly.oSu);
   CT* work = reinterpret_cast<CT*>(smem + Ly.oWork);
   auto WC = [&](int i) { return work + i * RMAX; };
-  CT* yball = reinterpret_cast<CT*>(smem + Ly.oYb);
-  CT* yb = yball + 32 * w;
+  // WY-apply partials (double-buffered per group) alias the residual scratch
+  constexpr int ZG = 9, QG = 4;  // warps of the Z group (rows <= 288) and Q group (cols <= 128)
+  CT* partZ = reinterpret_cast<CT*>(smem + Ly.oU);
+  CT* partQ = partZ + 2 * 32 * ZG;
   double* red = reinterpret_cast<double*>(smem + Ly.oRed);
   double* scal = reinterpret_cast<double*>(smem + Ly.oScal);
   int* iflag = reinterpret_cast<int*>(scal + S_FLAG);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(scal + S_MBAR);  // RQ full/empty, QR full/empty
   CT* rinvR = reinterpret_cast<CT*>(smem + Ly.oRinv);  // 1 / diag(R), u_s
   CT* rinvT = rinvR + CMAX;                             // 1 / diag(T11), u_s
   float* rinvRf = reinterpret_cast<float*>(rinvT + CMAX);  // u_f copies for the init
@@ -734,12 +811,20 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     t_last = globaltimer_ns();
     iflag[0] = 0;
     iflag[1] = -1;
+    for (int q = 0; q < 4 * NVB; q += 2 * NVB)
+      for (int b = 0; b < NVB; ++b) {
+        mbar_init(mbar + q + b, 32);       // full: the owner warp's lanes
+        mbar_init(mbar + q + NVB + b, NW);  // empty: one arrival per warp
+      }
   }
   // debug probe: raw globaltimer stamps of problem 0 at fixed points
   auto stamp = [&](int k) {
     if (a.stamps && pid == 0 && tid == 0) a.stamps[k] = globaltimer_ns();
   };
   stamp(0);
+  auto stampw = [&](int k, int W) {
+    if (a.stamps && pid == 0 && w == W && l == 0) a.stamps[k] = globaltimer_ns();
+  };
 
   // ---------------------------------------------------- pre-scaling (lse.hpp:314-329)
   double invA, invB;
@@ -836,24 +921,24 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
           const int i = w + NW * t, c = l + 32 * s;
           br[t][s] = (i < R && c < C) ? M[i + size_t(c) * ld] : 0.f;
         }
-      rq_slot<17>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<16>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<15>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<14>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<13>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<12>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<11>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<10>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<9>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<8>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<7>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<6>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<5>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<4>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<3>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<2>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<1>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
-      rq_slot<0>(br, m, n, p, C, w, l, vbuf, tau2, TQ);
+      rq_slot<17>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<16>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<15>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<14>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<13>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<12>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<11>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<10>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<9>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<8>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<7>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<6>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<5>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<4>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<3>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<2>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<1>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<0>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
       __syncthreads();
 #pragma unroll
       for (int t = 0; t < BT; ++t)
@@ -876,14 +961,14 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
           const int i = l + 32 * t, c = w + NW * s;
           ar[t][s] = (i < R && c < C) ? M[i + size_t(c) * ld] : 0.f;
         }
-      qr_slot<0>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
-      qr_slot<1>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
-      qr_slot<2>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
-      qr_slot<3>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
-      qr_slot<4>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
-      qr_slot<5>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
-      qr_slot<6>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
-      qr_slot<7>(ar, m, C, kz, w, l, vbuf, tau1, TZ);
+      qr_slot<0>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
+      qr_slot<1>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
+      qr_slot<2>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
+      qr_slot<3>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
+      qr_slot<4>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
+      qr_slot<5>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
+      qr_slot<6>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
+      qr_slot<7>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
       __syncthreads();
       stamp(3);
 #pragma unroll
@@ -898,10 +983,10 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   __syncthreads();
   if (w < Ly.nbz) {
     const int j0 = 32 * w;
-    build_T(TZ + w * 1024, tau1 + j0, (kz - j0) < 32 ? (kz - j0) : 32, l);
+    build_T(TZ + w * TSZ, tau1 + j0, (kz - j0) < 32 ? (kz - j0) : 32, l);
   } else if (w >= 8 && w - 8 < Ly.nbq) {
     const int b = w - 8, j0 = 32 * b;
-    build_T(TQ + b * 1024, tau2 + j0, (p - j0) < 32 ? (p - j0) : 32, l);
+    build_T(TQ + b * TSZ, tau2 + j0, (p - j0) < 32 ? (p - j0) : 32, l);
   } else if (w == 15) {
     // exact zero pivots of R, then of T11: the order in which the reference's
     // first failing trsv (lse.hpp:53 then :60) would throw singular_triangular
@@ -926,7 +1011,8 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     float* t4 = reinterpret_cast<float*>(WC(3));
     float* y = reinterpret_cast<float*>(WC(4));
     float* gf = reinterpret_cast<float*>(WC(5));
-    float* ybf = reinterpret_cast<float*>(yball) + 32 * w;
+    float* partZf = reinterpret_cast<float*>(smem + Ly.oU);
+    float* partQf = partZf + 2 * 32 * ZG;
     for (int i = tid; i < m; i += NT) {
       bf[i] = float(rinit[i]);
       c[i] = bf[i];
@@ -935,20 +1021,23 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     __syncthreads();
     if (w == 0) {
       trsv_up<float>(M, ld, m, n - p, p, rinvRf, y2, l);
-    } else if (w == 1) {
-      z_apply<float>(M, ld, kz, m, TZ, true, c, ybf, l);  // c = Z^T b
+    } else if (w >= NW - ZG) {
+      z_apply_mw<float>(M, ld, kz, m, TZ, true, c, partZf, Grp{w - (NW - ZG), ZG, l, 1});  // c = Z^T b
     }
     __syncthreads();
     if (iflag[0]) goto finish;
     gemv_rows<float, false>(M, ld, 0, k, k, p, y2, t4, tid, NT);
     __syncthreads();
-    if (w == 0) {
-      for (int i = l; i < k; i += 32) y[i] = c[i] - t4[i];
-      for (int i = l; i < p; i += 32) y[k + i] = y2[i];
-      __syncwarp();
-      trsv_up<float>(M, ld, 0, 0, k, rinvTf, y, l);
-      __syncwarp();
-      q_apply<float>(M, ld, p, m, n - p, n, TQ, true, y, ybf, l);  // x = Q^T [y1; y2]
+    if (w < QG) {
+      const Grp g{w, QG, l, 2};
+      if (w == 0) {
+        for (int i = l; i < k; i += 32) y[i] = c[i] - t4[i];
+        for (int i = l; i < p; i += 32) y[k + i] = y2[i];
+        __syncwarp();
+        trsv_up<float>(M, ld, 0, 0, k, rinvTf, y, l);
+      }
+      g.sync();
+      q_apply_mw<float>(M, ld, p, m, n - p, n, TQ, true, y, partQf, g);  // x = Q^T [y1; y2]
     }
     __syncthreads();
     if (iflag[0]) goto finish;
@@ -1027,9 +1116,9 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       const double sg = scal[S_RED0] == 0.0 ? 1.0 : scal[S_RED0];
       for (int j = tid; j < n; j += NT) gf[j] = float(cout[j] / sg);
       __syncthreads();
-      if (w == 0) {
-        q_apply<float>(M, ld, p, m, n - p, n, TQ, false, gf, ybf, l);  // Q g
-        trsv_upt<float>(M, ld, m, n - p, p, rinvRf, gf + (n - p), l);
+      if (w < QG) {
+        q_apply_mw<float>(M, ld, p, m, n - p, n, TQ, false, gf, partQf, Grp{w, QG, l, 2});  // Q g
+        if (w == 0) trsv_upt<float>(M, ld, m, n - p, p, rinvRf, gf + (n - p), l);
       }
       __syncthreads();
       if (iflag[0]) goto finish;
@@ -1177,12 +1266,15 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       for (int i = tid; i < m; i += NT) wv[i] = CT(rout[i] / sig);
       for (int i = tid; i < p; i += NT) y2[i] = CT(rout[m + i] / sig);
       __syncthreads();
-      if (w == 0) {
-        q_apply<CT>(M, ld, p, m, n - p, n, TQ, false, u, yb, l);  // u = Q f3
-      } else if (w == 1) {
-        z_apply<CT>(M, ld, kz, m, TZ, true, wv, yb, l);  // w = Z^T f1
-      } else if (w == 2) {
+      if (w < ZG) {
+        z_apply_mw<CT>(M, ld, kz, m, TZ, true, wv, partZ, Grp{w, ZG, l, 1});  // w = Z^T f1
+        if (pass == 1) stampw(16, 0);
+      } else if (w < ZG + QG) {
+        q_apply_mw<CT>(M, ld, p, m, n - p, n, TQ, false, u, partQ, Grp{w - ZG, QG, l, 2});  // u = Q f3
+        if (pass == 1) stampw(17, ZG);
+      } else if (w == ZG + QG) {
         trsv_up<CT>(M, ld, m, n - p, p, rinvR, y2, l);
+        if (pass == 1) stampw(18, ZG + QG);
       }
       __syncthreads();
       if (pass == 1) stamp(8);
@@ -1191,9 +1283,11 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
         for (int i = l; i < k; i += 32) q1[i] = u[i];
         __syncwarp();
         trsv_upt<CT>(M, ld, 0, 0, k, rinvT, q1, l);
+        if (pass == 1) stampw(23, 0);
       } else {
         gemv_rows<CT, false>(M, ld, 0, k, k, p, y2, t4, tid - 32, NT - 32);
         gemv_rows<CT, true>(M, ld, k, m - k, k, p, y2, t4 + k, tid - 32, NT - 32);
+        if (pass == 1) stampw(24, 1);
       }
       __syncthreads();
       if (pass == 1) stamp(9);
@@ -1209,16 +1303,22 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       }
       for (int i = tid; i < p; i += NT) y[k + i] = y2[i];
       __syncthreads();
-      if (w == 0) {
-        trsv_up<CT>(M, ld, 0, 0, k, rinvT, y, l);
-        __syncwarp();
-        q_apply<CT>(M, ld, p, m, n - p, n, TQ, true, y, yb, l);  // dx = Q^T y
-      } else if (w == 1) {
-        z_apply<CT>(M, ld, kz, m, TZ, false, dr, yb, l);  // dr = Z q
-      } else {
+      if (w < QG) {
+        const Grp g{w, QG, l, 2};
+        if (w == 0) trsv_up<CT>(M, ld, 0, 0, k, rinvT, y, l);
+        if (pass == 1) stampw(19, 0);
+        g.sync();
+        q_apply_mw<CT>(M, ld, p, m, n - p, n, TQ, true, y, partQ, g);  // dx = Q^T y
+        if (pass == 1) stampw(20, 0);
+      } else if (w < NW - ZG) {
         // s = T12^T q1 + (T22^T q2 - u2)  (q = wv)
-        gemv_cols<CT, false>(M, ld, 0, k, k, p, wv, t4, 2, NW - 2, w, l);
-        gemv_cols<CT, true>(M, ld, k, m - k, k, p, wv + k, q1, 2, NW - 2, w, l);
+        constexpr int NG = NW - ZG - QG;
+        gemv_cols<CT, false>(M, ld, 0, k, k, p, wv, t4, QG, NG, w, l);
+        gemv_cols<CT, true>(M, ld, k, m - k, k, p, wv + k, q1, QG, NG, w, l);
+        if (pass == 1) stampw(21, QG);
+      } else {
+        z_apply_mw<CT>(M, ld, kz, m, TZ, false, dr, partZ, Grp{w - (NW - ZG), ZG, l, 1});  // dr = Z q
+        if (pass == 1) stampw(22, NW - ZG);
       }
       __syncthreads();
       if (pass == 1) stamp(10);

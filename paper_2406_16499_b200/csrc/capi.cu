@@ -370,10 +370,12 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
   }
   DevBuf bstamps;
   const bool dbg = getenv("MLSB_DEBUG_STAMPS") != nullptr;
+  void* probe = nullptr;
   if (dbg) {
     if ((e = bstamps.alloc(64 * 8, st))) return cuda_fail(e, "cudaMallocAsync(stamps)");
     cudaMemsetAsync(bstamps.p, 0, 64 * 8, st);
     a.stamps = bstamps.as<unsigned long long>();
+    probe = mlsb::probe_buffer();
   }
   DevBuf bgws;
   if (m_global) {
@@ -413,6 +415,14 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
     for (int i = 1; i < 32; ++i)
       if (h[i]) fprintf(stderr, " [%d] %.1f", i, (h[i] - h[0]) * 1e-3);
     fprintf(stderr, "\n");
+    if (void* pp = probe) {
+      unsigned long long pr[128];
+      cudaMemcpy(pr, pp, sizeof(pr), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "MLSB_PROBE(cycles from warp 0 wait@40):");
+      for (int i = 64; i < 128; ++i)
+        if (pr[i]) fprintf(stderr, " [%d] %lld", i, (long long)(pr[i] - pr[64]));
+      fprintf(stderr, "\n");
+    }
 
   }
   return MLSB_OK;

@@ -51,6 +51,7 @@ cudaError_t launch_tile_solver(const TileArgs& a, cudaStream_t stream);
 
 // register-resident LSE tile solver (m + p <= 288, n <= 128, u_f = binary32,
 // u_r = binary64): BASELINE configs 1 and 4
+void* probe_buffer();  // debug (MLSB_PROBE builds): clock64 probe slots, or nullptr
 bool lse_reg_supported(int64_t m, int64_t n, int64_t p, int u_f, int u_s, int u_r,
                        size_t smem_limit);
 cudaError_t launch_lse_reg(const TileArgs& a, cudaStream_t stream);

@@ -168,15 +168,17 @@ __device__ __forceinline__ CT tsum32(const float (&v)[32], CT xv, int l) {
 }
 
 // One block of kb <= 32 reflectors applied to the entries [i0, i1) of x
-// (i1 - i0 <= 32 ngw, one entry per thread): x := x - V T' (V^T x).  The
-// thread's row of V stays in registers between the two products; V^T x is a
-// transposed warp reduction plus a fixed-order sum over the group's warps
-// (`part`, double-buffered by the caller, so one barrier per block).
+// (i1 <= 32 ngw): x := x - V T' (V^T x).  Thread t of the group owns entry t
+// (absolute index, the same for every block, so one block's update and the
+// next block's reads of x need no barrier between them).  The thread's row of
+// V stays in registers between the two products; V^T x is a transposed warp
+// reduction plus a fixed-order sum over the group's warps (`part`,
+// double-buffered by the caller, so one barrier per block).
 template <class CT, class VF>
 __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, const float* Tb,
                                          bool tr, CT* x, CT* part, const Grp& g) {
-  const int l = g.l, i = i0 + 32 * g.gw + l;
-  const bool act = i < i1;
+  const int l = g.l, i = 32 * g.gw + l;
+  const bool act = i >= i0 && i < i1;
   float v[32];
 #pragma unroll
   for (int q = 0; q < 32; ++q) v[q] = (act && q < kb) ? vf(i, q) : 0.f;
@@ -572,6 +574,14 @@ __device__ __forceinline__ void reduce16(float (&d)[16], int l) {
 // factorization).
 constexpr int NVB = 4;
 
+#ifdef MLSB_PROBE
+// debug: clock64 stamps of problem 0 inside QR steps 40/41 (slots 64..127)
+__device__ unsigned long long* g_probe = nullptr;
+#define PROBE(k) do { if (g_probe && blockIdx.x == 0) g_probe[k] = clock64(); } while (0)
+#else
+#define PROBE(k) do { } while (0)
+#endif
+
 // RQ owner path: apply reflector (vv, tj) to the owner's row slot TO, then
 // generate the next reflector (index jn, pivot pc, sequence number kn) from it.
 template <int TO>
@@ -675,6 +685,8 @@ __device__ __forceinline__ void qr_crit(float (&ar)[RT][CS], const float (&vr)[R
   for (int t = T0; t < RT; ++t)
     if (32 * t < m) dc = fmaf(ar[t][S1], vr[t], dc);
   dc = warp_sum(dc);
+  const int pb = (j1 == 41 || j1 == 42) && l == 0 ? 112 + 4 * (j1 - 41) : -1;
+  if (pb >= 0) PROBE(pb);
   if (tj != 0.f) {
     const float sc = tj * dc;
 #pragma unroll
@@ -683,9 +695,12 @@ __device__ __forceinline__ void qr_crit(float (&ar)[RT][CS], const float (&vr)[R
   }
   const int b = j1 % NVB;
   if (j1 >= NVB) mbar_wait(empty + b, ((j1 / NVB) - 1) & 1);
+  if (pb >= 0) PROBE(pb + 1);
   gen_col<S1>(ar, j1, m, l, vbuf + b * RMAX, tau1);
+  if (pb >= 0) PROBE(pb + 2);
   __syncwarp();
   mbar_arrive(full + b);
+  if (pb >= 0) PROBE(pb + 3);
 }
 
 // QR steps for the columns of slot SC (j = 16 SC + jw).  Column c is owned by
@@ -708,6 +723,7 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
     }
     const int b = j % NVB;
     mbar_wait(full + b, (j / NVB) & 1);
+    if ((j == 40 || j == 41) && l == 0) PROBE((j == 40 ? 64 : 96) + w);
     const float tj = tau1[j];
     const float* v = vbuf + b * RMAX;
     float vr[RT];
@@ -719,7 +735,7 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
       if (jw < NW - 1) qr_crit<SC, T0>(ar, vr, tj, j1, m, l, vbuf, tau1, full, empty);
       else qr_crit<(SC + 1 < CS ? SC + 1 : SC), T0>(ar, vr, tj, j1, m, l, vbuf, tau1, full, empty);
     }
-    const int bstart = j & ~31;
+    constexpr int bstart = NW * S0;  // j & ~31
     float d[CS];
 #pragma unroll
     for (int s = 0; s < CS; ++s) d[s] = 0.f;
@@ -732,30 +748,38 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
     __syncwarp();
     if (l == 0) mbar_arrive(empty + b);
     reduce8(d, l);
+    // slots S0..SC-1 hold finished columns of the current Gram block (c < j),
+    // slot SC holds column j (w == jw) with finished columns below it and live
+    // ones above, slots > SC hold live columns only
+    const bool upd = tj != 0.f;
 #pragma unroll
     for (int s = S0; s < CS; ++s) {
       const int c = w + NW * s;
-      if (c >= bstart && c < j) {
+      const bool gram = s < SC || (s == SC && w < jw);
+      const bool live = s > SC || (s == SC && w > jw);
+      if (gram) {
         if (l == 0) TZ[(bstart >> 5) * TSZ + (c - bstart) + TLD * (j - bstart)] = d[s];
-        continue;
-      }
-      if (c > j && c < C && tj != 0.f && !(own && c == j1)) {
+      } else if (live && upd && c < C && !(own && c == j1)) {
         const float sc = tj * d[s];
 #pragma unroll
         for (int t = T0; t < RT; ++t)
           if (32 * t < m) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
       }
     }
+    if (j == 40 && l == 0) PROBE(80 + w);
   }
 }
 
 // -------------------------------------------------------------- kernel
-template <class CT>
+// SM, SN, SP > 0: the problem shape is a compile-time constant (BASELINE
+// config 4: 256 x 128 x 32), so every row/column bound, the live slot ranges
+// and the active RQ slots fold away; 0: runtime shape.
+template <class CT, int SM = 0, int SN = 0, int SP = 0>
 __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
   const int64_t pid = blockIdx.x;
-  const int m = int(a.m), n = int(a.n), p = int(a.p);
+  const int m = SM > 0 ? SM : int(a.m), n = SN > 0 ? SN : int(a.n), p = SP > 0 ? SP : int(a.p);
   const Layout Ly = make_layout(m, n, p, sizeof(CT));
   const int R = Ly.R, C = Ly.C, ld = Ly.ld, kz = Ly.kz;
   constexpr bool LOWS = sizeof(CT) == 4;
@@ -1377,7 +1401,8 @@ finish:
 template <class CT>
 static cudaError_t launch_ct(const TileArgs& a, cudaStream_t st) {
   const Layout L = make_layout(a.m, a.n, a.p, sizeof(CT));
-  auto kern = lse_reg_kernel<CT>;
+  auto kern = (a.m == 256 && a.n == 128 && a.p == 32) ? lse_reg_kernel<CT, 256, 128, 32>
+                                                      : lse_reg_kernel<CT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(L.total));
   if (e != cudaSuccess) return e;
@@ -1386,6 +1411,21 @@ static cudaError_t launch_ct(const TileArgs& a, cudaStream_t st) {
 }
 
 }  // namespace reg
+
+// debug probe buffer (MLSB_PROBE builds only): 128 clock64 slots, zeroed
+void* probe_buffer() {
+#ifdef MLSB_PROBE
+  static unsigned long long* buf = nullptr;
+  if (!buf) {
+    cudaMalloc(&buf, 128 * 8);
+    cudaMemcpyToSymbol(reg::g_probe, &buf, sizeof(buf));
+  }
+  cudaMemset(buf, 0, 128 * 8);
+  return buf;
+#else
+  return nullptr;
+#endif
+}
 
 bool lse_reg_supported(int64_t m, int64_t n, int64_t p, int u_f, int u_s, int u_r,
                        size_t smem_limit) {

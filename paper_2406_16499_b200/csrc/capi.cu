@@ -418,9 +418,12 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
     if (void* pp = probe) {
       unsigned long long pr[128];
       cudaMemcpy(pr, pp, sizeof(pr), cudaMemcpyDeviceToHost);
-      fprintf(stderr, "MLSB_PROBE(cycles from warp 0 wait@40):");
-      for (int i = 64; i < 128; ++i)
-        if (pr[i]) fprintf(stderr, " [%d] %lld", i, (long long)(pr[i] - pr[64]));
+      fprintf(stderr, "MLSB_PROBE per QR step j1 (owner warp): sum/upd/gen/pub cycles after previous publish\n");
+      for (int i = 1; i < 32; ++i)
+        if (pr[i] && pr[96 + i - 1])
+          fprintf(stderr, "  j1=%d w%d: %lld %lld %lld %lld\n", 33 + i, (33 + i) & 15,
+                  (long long)(pr[i] - pr[96 + i - 1]), (long long)(pr[32 + i] - pr[96 + i - 1]),
+                  (long long)(pr[64 + i] - pr[96 + i - 1]), (long long)(pr[96 + i] - pr[96 + i - 1]));
       fprintf(stderr, "\n");
     }
 

@@ -83,43 +83,37 @@ enum Slot { S_SA = 0, S_SB, S_CB, S_CD, S_NB, S_ND, S_NA, S_NBF, S_SIG, S_BETA, 
             S_RED0 = 16, S_FLAG = 40, S_MBAR = 48 };
 
 // ---------------------------------------------------------------- helpers
-// 8 partial sums per lane -> lane-complete sums (8-way transposed butterfly:
-// 4+2+1+1+1 exchanges, then 8 broadcasts).  Every lane returns all 8 sums.
-struct F8 {
-  float d[8];
-};
-__device__ __forceinline__ F8 reduce8_core(F8 in, int l) {
-  float (&d)[8] = in.d;
-  const bool b4 = l & 16, b3 = l & 8, b2 = l & 4;
+
+// Transposed butterfly over the N = 2^k live entries d[S0 .. S0+N-1] of 8
+// per-lane partial sums: k pair-halving exchanges, 5 - k plain exchanges,
+// then N broadcasts; every lane returns all N sums (fixed order).
+template <int S0, int N>
+__device__ __forceinline__ void reduce_live(float (&d)[8], int l) {
+  static_assert(N == 8 || N == 4 || N == 2, "N");
+  float e[N];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float send = b4 ? d[i] : d[i + 4], keep = b4 ? d[i + 4] : d[i];
-    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  for (int i = 0; i < N; ++i) e[i] = d[S0 + i < 8 ? S0 + i : 7];
+  int h = N / 2;
+#pragma unroll
+  for (int lv = 0; lv < 3; ++lv) {
+    if ((N >> lv) >= 2) {
+      const int hh = N >> (lv + 1);
+      const bool b = l & (16 >> lv);
+#pragma unroll
+      for (int i = 0; i < hh; ++i) {
+        const float send = b ? e[i] : e[i + hh], keep = b ? e[i + hh] : e[i];
+        e[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16 >> lv);
+      }
+    }
   }
+  (void)h;
+  constexpr int K = N == 8 ? 3 : (N == 4 ? 2 : 1);
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const float send = b3 ? d[i] : d[i + 2], keep = b3 ? d[i + 2] : d[i];
-    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  {
-    const float send = b2 ? d[0] : d[1], keep = b2 ? d[1] : d[0];
-    d[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  d[0] += __shfl_xor_sync(0xffffffffu, d[0], 2);
-  d[0] += __shfl_xor_sync(0xffffffffu, d[0], 1);
-  // lane l now holds the sum of value index (l >> 2) & 7
-  const float mine = d[0];
+  for (int o = 16 >> K; o >= 1; o >>= 1) e[0] += __shfl_xor_sync(0xffffffffu, e[0], o);
+  const float mine = e[0];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) d[s] = __shfl_sync(0xffffffffu, mine, s << 2);
-  return in;
-}
-__device__ __forceinline__ void reduce8(float (&d)[8], int l) {
-  F8 x;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) x.d[i] = d[i];
-  x = reduce8_core(x, l);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) d[i] = x.d[i];
+  for (int q = 0; q < N; ++q)
+    if (S0 + q < 8) d[S0 + q] = __shfl_sync(0xffffffffu, mine, q << (5 - K));
 }
 
 // ------------------------------------------- multi-warp WY block applies
@@ -403,21 +397,53 @@ __device__ void build_T(float* G, const float* tau, int kb, int l) {
   __syncwarp();
 }
 
-// xLARFG (householder.hpp:30-53).  ||x||^2 is accumulated in binary64 as in the
-// reference; beta, tau and 1/(alpha - beta) -- which the reference rounds to
-// binary32 anyway -- are formed with correctly rounded binary32 sqrt/div/rcp,
-// which keeps the three long-latency fp64 operations off the critical path of
-// every reflector step (a few ulps of u_f, well inside the factorization error).
-__device__ __forceinline__ void larfg(float alpha, double ss, float& tj, float& inv, float& beta) {
+// xLARFG (householder.hpp:30-53) from alpha and a2ss = alpha^2 + ||x||^2.
+// beta, tau and 1/(alpha - beta) -- which the reference rounds to binary32
+// anyway -- come from correctly rounded binary32 sqrt and reciprocals, which
+// keeps the long-latency binary64 operations off the critical path of every
+// reflector step (a few ulps of u_f, well inside the factorization error).
+__device__ __forceinline__ void larfg(float alpha, bool nonzero, float a2ss, float& tj, float& inv,
+                                      float& beta) {
   tj = 0.f;
   inv = 1.f;
   beta = alpha;
-  if (ss != 0.0) {
-    const float nrm = __fsqrt_rn(float(fma(double(alpha), double(alpha), ss)));
-    const float bt = -copysignf(nrm, alpha);
-    tj = __fdiv_rn(__fsub_rn(bt, alpha), bt);
+  if (nonzero) {
+    const float bt = -copysignf(__fsqrt_rn(a2ss), alpha);
+    const float rb = __frcp_rn(bt);
     inv = __frcp_rn(__fsub_rn(alpha, bt));
+    tj = __fmul_rn(__fsub_rn(bt, alpha), rb);
     beta = bt;
+  }
+}
+
+// ||x||^2 of a reflector tail held as per-lane partial sums.  The reference
+// accumulates it in binary64 (householder.hpp:32-34); here the squares are
+// summed in binary32 (two chains per lane + a 5-level butterfly: relative
+// error ~1e-7, far below the u_f-level factorization error) and the binary64
+// sum is redone only when the result is tiny (< 2^-100, where binary32
+// squares start to lose bits to underflow).  Warp-uniform.
+template <int K, class Pred>
+__device__ __forceinline__ void tail_norm(const float (&v)[K], const Pred& live, float alpha,
+                                          bool& nonzero, float& a2ss) {
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int t = 0; t < K; ++t)
+    if (live(t)) {
+      if (t & 1) s1 = fmaf(v[t], v[t], s1);
+      else s0 = fmaf(v[t], v[t], s0);
+    }
+  const float ssf = warp_sum(s0 + s1);
+  if (ssf >= 0x1p-100f || !(ssf == ssf)) {
+    nonzero = ssf != 0.f;
+    a2ss = fmaf(alpha, alpha, ssf);
+  } else {
+    double sd = 0.0;
+#pragma unroll
+    for (int t = 0; t < K; ++t)
+      if (live(t)) sd = fma(double(v[t]), double(v[t]), sd);
+    sd = warp_sum(sd);
+    nonzero = sd != 0.0;
+    a2ss = float(fma(double(alpha), double(alpha), sd));
   }
 }
 
@@ -430,19 +456,16 @@ struct Col9 {
 };
 __device__ __forceinline__ Col9 gen_col_core(Col9 col, int jc, int t0, int m, int l, float* vout,
                                           float* tau1) {
-  double ss = 0.0;
-#pragma unroll
-  for (int t = 0; t < RT; ++t) {
-    const int i = l + 32 * t;
-    if (t >= t0 && i > jc && i < m) ss = fma(double(col.v[t]), double(col.v[t]), ss);
-  }
-  ss = warp_sum(ss);
   float a9 = 0.f;
 #pragma unroll
   for (int t = 0; t < RT; ++t) a9 = (t == (jc >> 5)) ? col.v[t] : a9;
   const float alpha = __shfl_sync(0xffffffffu, a9, jc & 31);
+  bool nz;
+  float a2ss;
+  tail_norm(col.v, [&](int t) { const int i = l + 32 * t; return t >= t0 && i > jc && i < m; },
+            alpha, nz, a2ss);
   float tj, inv, beta;
-  larfg(alpha, ss, tj, inv, beta);
+  larfg(alpha, nz, a2ss, tj, inv, beta);
 #pragma unroll
   for (int t = 0; t < RT; ++t) {
     const int i = l + 32 * t;
@@ -482,19 +505,15 @@ struct Row4 {
 };
 __device__ __forceinline__ Row4 gen_row_core(Row4 row, int j, int pc, int C, int l, float* vout,
                                           float* tau2) {
-  double ss = 0.0;
-#pragma unroll
-  for (int s = 0; s < BS; ++s) {
-    const int c = l + 32 * s;
-    if (c < pc) ss = fma(double(row.v[s]), double(row.v[s]), ss);
-  }
-  ss = warp_sum(ss);
   float a4 = 0.f;
 #pragma unroll
   for (int s = 0; s < BS; ++s) a4 = (s == (pc >> 5)) ? row.v[s] : a4;
   const float alpha = __shfl_sync(0xffffffffu, a4, pc & 31);
+  bool nz;
+  float a2ss;
+  tail_norm(row.v, [&](int s) { return l + 32 * s < pc; }, alpha, nz, a2ss);
   float tj, inv, beta;
-  larfg(alpha, ss, tj, inv, beta);
+  larfg(alpha, nz, a2ss, tj, inv, beta);
 #pragma unroll
   for (int s = 0; s < BS; ++s) {
     const int c = l + 32 * s;
@@ -588,6 +607,8 @@ template <int TO>
 __device__ __forceinline__ void rq_crit(float (&br)[BT][BS], const float (&vv)[BS], float tj, int jn,
                                         int pc, int C, int l, float* vbuf, float* tau2,
                                         uint64_t* full, uint64_t* empty, int kn) {
+  const int b = kn % NVB;
+  if (kn >= NVB) mbar_wait(empty + b, ((kn / NVB) - 1) & 1);  // (long satisfied: off the chain)
   float dc = 0.f;
 #pragma unroll
   for (int s = 0; s < BS; ++s) dc = fmaf(br[TO][s], vv[s], dc);
@@ -595,11 +616,9 @@ __device__ __forceinline__ void rq_crit(float (&br)[BT][BS], const float (&vv)[B
   if (tj != 0.f)
 #pragma unroll
     for (int s = 0; s < BS; ++s) br[TO][s] = fmaf(-(tj * vv[s]), dc, br[TO][s]);
-  const int b = kn % NVB;
-  if (kn >= NVB) mbar_wait(empty + b, ((kn / NVB) - 1) & 1);
   gen_row<TO>(br, jn, pc, C, l, vbuf + b * CMAX, tau2);
-  __syncwarp();
-  mbar_arrive(full + b);
+  __syncwarp();  // orders the warp's stores of v and tau before lane 0's release
+  if (l == 0) mbar_arrive(full + b);
 }
 
 // RQ steps for the reflector rows of row slot TO (rows 16 TO + 15 ... 16 TO),
@@ -621,7 +640,7 @@ __device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p
     if (k == 0 && w == wo) {
       gen_row<TO>(br, j, n - p + j, C, l, vbuf, tau2);
       __syncwarp();
-      mbar_arrive(full);
+      if (l == 0) mbar_arrive(full);
     }
     mbar_wait(full + b, (k / NVB) & 1);
     const float tj = tau2[j];
@@ -658,15 +677,20 @@ __device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p
     e0 = warp_sum(e0);
     e1 = warp_sum(e1);
     const int jb = j & ~31;
+    // rows above the reflector row are updated (the owner's row - 1 already
+    // was); rows below it only give Gram entries.  tj == 0 means v = e_pc, whose
+    // update adds exact zeros, so the update is branch-free.
 #pragma unroll
     for (int t = 0; t < BT; ++t) {
       const int i = w + NW * t;
       const float dt = t < 16 ? d[t < 16 ? t : 0] : (t == 16 ? e0 : e1);
-      if (i < row) {
-        if (tj != 0.f && !(own && i == row - 1))
+      const bool above = t < TO || (t == TO && w < wo);
+      const bool below = t > TO || (t == TO && w > wo);
+      const bool skip = own && (t == TO ? wo > 0 : (t == TO - 1 && wo == 0));
+      if (above && !skip) {
 #pragma unroll
-          for (int s = 0; s < BS; ++s) br[t][s] = fmaf(-(tj * vv[s]), dt, br[t][s]);
-      } else if (i > row && i < m + p) {
+        for (int s = 0; s < BS; ++s) br[t][s] = fmaf(-(tj * vv[s]), dt, br[t][s]);
+      } else if (below && i < m + p) {
         const int kk = i - m;
         if (l == 0 && (kk & ~31) == jb) TQ[(jb >> 5) * TSZ + (j - jb) + TLD * (kk - jb)] = dt;
       }
@@ -680,12 +704,16 @@ template <int S1, int T0>
 __device__ __forceinline__ void qr_crit(float (&ar)[RT][CS], const float (&vr)[RT], float tj, int j1,
                                         int m, int l, float* vbuf, float* tau1, uint64_t* full,
                                         uint64_t* empty) {
+  const int b = j1 % NVB;
+  if (j1 >= NVB) mbar_wait(empty + b, ((j1 / NVB) - 1) & 1);  // (long satisfied: off the chain)
   float dc = 0.f;
 #pragma unroll
   for (int t = T0; t < RT; ++t)
     if (32 * t < m) dc = fmaf(ar[t][S1], vr[t], dc);
   dc = warp_sum(dc);
-  const int pb = (j1 == 41 || j1 == 42) && l == 0 ? 112 + 4 * (j1 - 41) : -1;
+  // probe layout (steps j1 = 33..64): [j1-33] warp_sum done, [32+..] update done,
+  // [64+..] gen done, [96+..] published
+  const int pb = (j1 >= 33 && j1 < 65 && l == 0) ? j1 - 33 : -1;
   if (pb >= 0) PROBE(pb);
   if (tj != 0.f) {
     const float sc = tj * dc;
@@ -693,14 +721,12 @@ __device__ __forceinline__ void qr_crit(float (&ar)[RT][CS], const float (&vr)[R
     for (int t = T0; t < RT; ++t)
       if (32 * t < m) ar[t][S1] = fmaf(-sc, vr[t], ar[t][S1]);
   }
-  const int b = j1 % NVB;
-  if (j1 >= NVB) mbar_wait(empty + b, ((j1 / NVB) - 1) & 1);
-  if (pb >= 0) PROBE(pb + 1);
+  if (pb >= 0) PROBE(pb + 32);
   gen_col<S1>(ar, j1, m, l, vbuf + b * RMAX, tau1);
-  if (pb >= 0) PROBE(pb + 2);
-  __syncwarp();
-  mbar_arrive(full + b);
-  if (pb >= 0) PROBE(pb + 3);
+  if (pb >= 0) PROBE(pb + 64);
+  __syncwarp();  // orders the warp's stores of v and tau before lane 0's release
+  if (l == 0) mbar_arrive(full + b);
+  if (pb >= 0) PROBE(pb + 96);
 }
 
 // QR steps for the columns of slot SC (j = 16 SC + jw).  Column c is owned by
@@ -719,11 +745,10 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
     if (SC == 0 && j == 0 && w == 0) {
       gen_col<0>(ar, 0, m, l, vbuf, tau1);
       __syncwarp();
-      mbar_arrive(full);
+      if (l == 0) mbar_arrive(full);
     }
     const int b = j % NVB;
     mbar_wait(full + b, (j / NVB) & 1);
-    if ((j == 40 || j == 41) && l == 0) PROBE((j == 40 ? 64 : 96) + w);
     const float tj = tau1[j];
     const float* v = vbuf + b * RMAX;
     float vr[RT];
@@ -747,26 +772,29 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
     }
     __syncwarp();
     if (l == 0) mbar_arrive(empty + b);
-    reduce8(d, l);
+    constexpr int NL = CS - S0 > 4 ? 8 : (CS - S0 > 2 ? 4 : 2);
+    reduce_live<(CS - NL > S0 ? S0 : CS - NL), NL>(d, l);
     // slots S0..SC-1 hold finished columns of the current Gram block (c < j),
     // slot SC holds column j (w == jw) with finished columns below it and live
-    // ones above, slots > SC hold live columns only
-    const bool upd = tj != 0.f;
+    // ones above, slots > SC hold live columns only.  The owner already updated
+    // column j1 (slot SC, or SC + 1 when jw is the last warp).  tj == 0 means
+    // v = e_j, whose update adds exact zeros, so the update is branch-free.
+    const bool own_sc = own && jw < NW - 1, own_sc1 = own && jw == NW - 1;
 #pragma unroll
     for (int s = S0; s < CS; ++s) {
       const int c = w + NW * s;
       const bool gram = s < SC || (s == SC && w < jw);
-      const bool live = s > SC || (s == SC && w > jw);
+      const bool live = s > SC + 1 || (s == SC && w > jw && !own_sc) || (s == SC + 1 && !own_sc1);
+      const bool cok = NW * (s + 1) <= C || c < C;
       if (gram) {
         if (l == 0) TZ[(bstart >> 5) * TSZ + (c - bstart) + TLD * (j - bstart)] = d[s];
-      } else if (live && upd && c < C && !(own && c == j1)) {
+      } else if (live && cok) {
         const float sc = tj * d[s];
 #pragma unroll
         for (int t = T0; t < RT; ++t)
           if (32 * t < m) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
       }
     }
-    if (j == 40 && l == 0) PROBE(80 + w);
   }
 }
 
@@ -837,7 +865,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     iflag[1] = -1;
     for (int q = 0; q < 4 * NVB; q += 2 * NVB)
       for (int b = 0; b < NVB; ++b) {
-        mbar_init(mbar + q + b, 32);       // full: the owner warp's lanes
+        mbar_init(mbar + q + b, 1);        // full: the owner warp's lane 0
         mbar_init(mbar + q + NVB + b, NW);  // empty: one arrival per warp
       }
   }

@@ -175,7 +175,10 @@ __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, c
   const bool act = i >= i0 && i < i1;
   float v[32];
 #pragma unroll
-  for (int q = 0; q < 32; ++q) v[q] = (act && q < kb) ? vf(i, q) : 0.f;
+  for (int q = 0; q < 32; ++q) {
+    const float vq = vf(i, q);  // branch-free (clamped) load
+    v[q] = (act && q < kb) ? vq : 0.f;
+  }
   const CT xi = act ? x[i] : CT(0);
   part[32 * g.gw + l] = tsum32(v, xi, l);
   g.sync();
@@ -187,7 +190,8 @@ __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, c
   for (int k = 0; k < 32; ++k) {
     const CT yk = __shfl_sync(0xffffffffu, y, k);
     const bool use = k < kb && (tr ? k <= l : k >= l);
-    const float t = use ? (tr ? Tb[k + TLD * l] : Tb[l + TLD * k]) : 0.f;
+    const float tv = Tb[tr ? k + TLD * l : l + TLD * k];
+    const float t = use ? tv : 0.f;
     if (k & 1) z1 += CT(t) * yk;
     else z0 += CT(t) * yk;
   }
@@ -204,20 +208,24 @@ __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, c
 // QR (Z) reflectors: v_q = e_{j0+q} + M[j0+q+1 : rend, j0+q]; entry index = row
 struct ZV {
   const float* M;
-  int ld, j0;
+  int ld, j0, rmax, cmax;  // clamps keep the (unconditional) load inside M
   __device__ __forceinline__ float operator()(int r, int q) const {
     const int d = r - j0;
-    return d > q ? M[r + size_t(j0 + q) * ld] : (d == q ? 1.f : 0.f);
+    const int rr = r < rmax ? r : rmax, cc = j0 + q < cmax ? j0 + q : cmax;
+    const float mv = M[rr + size_t(cc) * ld];
+    return d > q ? mv : (d == q ? 1.f : 0.f);
   }
 };
 // RQ (Q) reflectors in rows rtop + j: entries at columns c < ptop + j, unit at
 // c = ptop + j; entry index = column
 struct QV {
   const float* M;
-  int ld, row0, pc0;  // row0 = rtop + j0, pc0 = ptop + j0
+  int ld, row0, pc0, rmax, cmax;  // row0 = rtop + j0, pc0 = ptop + j0; load clamps
   __device__ __forceinline__ float operator()(int c, int q) const {
     const int pc = pc0 + q;
-    return c < pc ? M[(row0 + q) + size_t(c) * ld] : (c == pc ? 1.f : 0.f);
+    const int rr = row0 + q < rmax ? row0 + q : rmax, cc = c < cmax ? c : cmax;
+    const float mv = M[rr + size_t(cc) * ld];
+    return c < pc ? mv : (c == pc ? 1.f : 0.f);
   }
 };
 
@@ -231,7 +239,8 @@ __device__ void z_apply_mw(const float* M, int ld, int k, int rend, const float*
   for (int s = 0; s < nb; ++s) {
     const int b = herm ? s : nb - 1 - s;
     const int j0 = 32 * b, kb = (k - j0) < 32 ? (k - j0) : 32;
-    wy_block(ZV{M, ld, j0}, j0, rend, kb, TZ + b * TSZ, herm, x, part + (s & 1) * 32 * g.ngw, g);
+    wy_block(ZV{M, ld, j0, ld - 1, k - 1}, j0, rend, kb, TZ + b * TSZ, herm, x,
+             part + (s & 1) * 32 * g.ngw, g);
   }
 }
 
@@ -244,8 +253,8 @@ __device__ void q_apply_mw(const float* M, int ld, int kq, int rtop, int ptop, i
     const int b = herm ? s : nb - 1 - s;
     const int j0 = 32 * b, kb = (kq - j0) < 32 ? (kq - j0) : 32;
     const int cmax = (ptop + j0 + kb) < dim ? (ptop + j0 + kb) : dim;
-    wy_block(QV{M, ld, rtop + j0, ptop + j0}, 0, cmax, kb, TQ + b * TSZ, herm, x,
-             part + (s & 1) * 32 * g.ngw, g);
+    wy_block(QV{M, ld, rtop + j0, ptop + j0, rtop + kq - 1, dim - 1}, 0, cmax, kb, TQ + b * TSZ,
+             herm, x, part + (s & 1) * 32 * g.ngw, g);
   }
 }
 
@@ -264,7 +273,11 @@ __device__ void trsv_up(const float* M, int ld, int r0, int c0, int k, const CT*
     float urow[32];
 #pragma unroll
     for (int jj = 0; jj < 32; ++jj)
-      urow[jj] = (jj < bs && l < jj) ? M[(r0 + i0 + l) + size_t(c0 + i0 + jj) * ld] : 0.f;
+    {
+      const int ll = l < bs ? l : bs - 1, jc = jj < bs ? jj : bs - 1;  // branch-free loads
+      const float u = M[(r0 + i0 + ll) + size_t(c0 + i0 + jc) * ld];
+      urow[jj] = (jj < bs && l < jj) ? u : 0.f;
+    }
     CT xi = l < bs ? x[i0 + l] : CT(0);
     const CT ri = l < bs ? rinv[i0 + l] : CT(0);
 #pragma unroll
@@ -296,7 +309,11 @@ __device__ void trsv_upt(const float* M, int ld, int r0, int c0, int k, const CT
     float ucol[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      ucol[j] = (j < bs && j < l && l < bs) ? M[(r0 + i0 + j) + size_t(c0 + i0 + l) * ld] : 0.f;
+    {
+      const int ll = l < bs ? l : bs - 1, jr = j < bs ? j : bs - 1;  // branch-free loads
+      const float u = M[(r0 + i0 + jr) + size_t(c0 + i0 + ll) * ld];
+      ucol[j] = (j < bs && j < l && l < bs) ? u : 0.f;
+    }
     CT xi = l < bs ? x[i0 + l] : CT(0);
     const CT ri = l < bs ? rinv[i0 + l] : CT(0);
 #pragma unroll

@@ -109,6 +109,21 @@ int mlsb_mpgls(const double* W, int64_t ldw, const double* V, int64_t ldv, const
                int64_t n, int64_t m, int64_t p, const mlsb_config* cfg, double* x, double* y,
                double* z, mlsb_trace* trace, int64_t* singular_index, const mlsb_exec* exec);
 
+/* binary64 direct solvers: the err-2 / er-2 reference of the experiment
+ * harness (detail::lse_direct_reference / gls_direct_reference,
+ * inc/experiment.hpp:50-73, over lse_direct inc/lse.hpp:132-152 and
+ * gls_direct inc/gls.hpp:85-91).  GRQ / GQR and the null-space solve at
+ * binary64 (no pre-scaling, no refinement); LSE r = b - A x and v from
+ * R^T v = (Q A^T r)(n-p:n), GLS z = Q [0; T22^-T (Z y)(k:p)] -- the same
+ * quantities the reference forms through the factors.  Zero pivots give
+ * MLSB_ERR_SINGULAR with the reference's index. */
+int mlsb_lse_direct(const double* A, int64_t lda, const double* B, int64_t ldb, const double* b,
+                    const double* d, int64_t m, int64_t n, int64_t p, double* x, double* r,
+                    double* v, int64_t* singular_index, const mlsb_exec* exec);
+int mlsb_gls_direct(const double* W, int64_t ldw, const double* V, int64_t ldv, const double* d,
+                    int64_t n, int64_t m, int64_t p, double* x, double* y, double* z,
+                    int64_t* singular_index, const mlsb_exec* exec);
+
 /* Complex128 problems (interleaved re, im; same shapes and semantics with
  * Hermitian transposes), solved with complex64 factors at u_f = low.  The
  * reference is real-only; these serve BASELINE config 5. */

@@ -118,5 +118,39 @@ inline mpgls_result mpgls(const gls_problem& pb, const refinement_config& cfg) {
   return out;
 }
 
+// GPU drop-in for detail::lse_direct_reference (inc/experiment.hpp:50-59):
+// binary64 factorization + direct solve, the err-2 reference
+inline lse_state lse_direct_reference(const lse_problem& pb) {
+  pb.validate();
+  const auto m = static_cast<int64_t>(pb.m()), n = static_cast<int64_t>(pb.n()),
+             p = static_cast<int64_t>(pb.p());
+  lse_state st;
+  st.x.assign(n, 0.0);
+  st.r.assign(m, 0.0);
+  st.v.assign(p, 0.0);
+  int64_t sing = -1;
+  const int rc = mlsb_lse_direct(pb.A.data().data(), m, pb.B.data().data(), p, pb.b.data(),
+                                 pb.d.data(), m, n, p, st.x.data(), st.r.data(), st.v.data(), &sing,
+                                 nullptr);
+  detail::throw_for(rc, sing);
+  return st;
+}
+
+// GPU drop-in for detail::gls_direct_reference (inc/experiment.hpp:65-73)
+inline gls_state gls_direct_reference(const gls_problem& pb) {
+  pb.validate();
+  const auto n = static_cast<int64_t>(pb.n()), m = static_cast<int64_t>(pb.m()),
+             p = static_cast<int64_t>(pb.p());
+  gls_state st;
+  st.x.assign(m, 0.0);
+  st.y.assign(p, 0.0);
+  st.z.assign(n, 0.0);
+  int64_t sing = -1;
+  const int rc = mlsb_gls_direct(pb.W.data().data(), n, pb.V.data().data(), n, pb.d.data(), n, m,
+                                 p, st.x.data(), st.y.data(), st.z.data(), &sing, nullptr);
+  detail::throw_for(rc, sing);
+  return st;
+}
+
 }  // namespace b200
 }  // namespace mixedls

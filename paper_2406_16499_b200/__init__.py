@@ -44,6 +44,8 @@ from .api import (  # noqa: F401
     PrecisionConfig,
     RefinementConfig,
     RefinementTrace,
+    gls_direct,
+    lse_direct,
     mpgls,
     mpgls_batched,
     mplse,
@@ -53,6 +55,6 @@ from .api import (  # noqa: F401
 __all__ = [
     "LseProblem", "GlsProblem", "LseState", "GlsState", "PrecisionConfig", "RefinementConfig",
     "RefinementTrace", "MplseResult", "MpglsResult", "mplse", "mpgls", "mplse_batched",
-    "mpgls_batched", "MixedlsError", "DimensionError", "InvalidInput", "SingularTriangular",
+    "mpgls_batched", "lse_direct", "gls_direct", "MixedlsError", "DimensionError", "InvalidInput", "SingularTriangular",
     "CudaError", "Unsupported", "lib", "lib_path",
 ]

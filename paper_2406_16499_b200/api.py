@@ -231,6 +231,73 @@ def mpgls(pb: GlsProblem, cfg: RefinementConfig | None = None, stream=None) -> M
     return MpglsResult(GlsState(x, y, z), _trace_from(tr, hist))
 
 
+def lse_direct(pb: LseProblem, stream=None) -> LseState:
+    """binary64 direct LSE solve on the GPU: the err-2 reference of the experiment
+    harness (detail::lse_direct_reference, inc/experiment.hpp:50-59)."""
+    dev = _is_cuda(pb.A)
+    if dev:
+        import torch
+
+        A, B, b, d = pb.A, pb.B, pb.b, pb.d
+        m, n, lda = _matrix_ld(A)
+        p, _, ldb = _matrix_ld(B)
+        x = torch.empty(n, dtype=torch.float64, device=A.device)
+        r = torch.empty(m, dtype=torch.float64, device=A.device)
+        v = torch.empty(p, dtype=torch.float64, device=A.device)
+    else:
+        A = np.asfortranarray(pb.A, dtype=np.float64)
+        B = np.asfortranarray(pb.B, dtype=np.float64)
+        if A.ndim != 2 or B.ndim != 2 or B.shape[1] != A.shape[1]:
+            raise _capi.DimensionError("lse_problem: A and B column counts differ")
+        b = np.ascontiguousarray(pb.b, dtype=np.float64)
+        d = np.ascontiguousarray(pb.d, dtype=np.float64)
+        m, n = A.shape
+        p = B.shape[0]
+        if b.shape != (m,) or d.shape != (p,):
+            raise _capi.DimensionError("lse_problem: rhs length mismatch")
+        lda, ldb = max(m, 1), max(p, 1)
+        x, r, v = np.zeros(n), np.zeros(m), np.zeros(p)
+    sing = C.c_int64(-1)
+    ex = _exec(dev, stream)
+    rc = lib.mlsb_lse_direct(_ptr(A), lda, _ptr(B), ldb, _ptr(b), _ptr(d), m, n, p, _ptr(x),
+                             _ptr(r), _ptr(v), C.byref(sing), C.byref(ex))
+    raise_for(rc, sing.value)
+    return LseState(x, r, v)
+
+
+def gls_direct(pb: GlsProblem, stream=None) -> GlsState:
+    """binary64 direct GLS solve on the GPU: the er-2 reference of the experiment
+    harness (detail::gls_direct_reference, inc/experiment.hpp:65-73)."""
+    dev = _is_cuda(pb.W)
+    if dev:
+        import torch
+
+        W, V, d = pb.W, pb.V, pb.d
+        n, m, ldw = _matrix_ld(W)
+        _, p, ldv = _matrix_ld(V)
+        x = torch.empty(m, dtype=torch.float64, device=W.device)
+        y = torch.empty(p, dtype=torch.float64, device=W.device)
+        z = torch.empty(n, dtype=torch.float64, device=W.device)
+    else:
+        W = np.asfortranarray(pb.W, dtype=np.float64)
+        V = np.asfortranarray(pb.V, dtype=np.float64)
+        if W.ndim != 2 or V.ndim != 2 or V.shape[0] != W.shape[0]:
+            raise _capi.DimensionError("gls_problem: W and V row counts differ")
+        d = np.ascontiguousarray(pb.d, dtype=np.float64)
+        n, m = W.shape
+        p = V.shape[1]
+        if d.shape != (n,):
+            raise _capi.DimensionError("gls_problem: rhs length mismatch")
+        ldw = ldv = max(n, 1)
+        x, y, z = np.zeros(m), np.zeros(p), np.zeros(n)
+    sing = C.c_int64(-1)
+    ex = _exec(dev, stream)
+    rc = lib.mlsb_gls_direct(_ptr(W), ldw, _ptr(V), ldv, _ptr(d), n, m, p, _ptr(x), _ptr(y),
+                             _ptr(z), C.byref(sing), C.byref(ex))
+    raise_for(rc, sing.value)
+    return GlsState(x, y, z)
+
+
 # ---------------------------------------------------------------------------
 @dataclass
 class BatchResult:

@@ -548,6 +548,40 @@ int mlsb_mpgls(const double* W, int64_t ldw, const double* V, int64_t ldv, const
                       singular_index, exec);
 }
 
+// binary64 direct solvers: the initial solve of the refinement at
+// u_f = u_s = u = u_r = working with zero refinement passes.
+static mlsb_config direct_config() {
+  mlsb_config c = mlsb_default_config();
+  c.u_f = c.u_s = c.u = c.u_r = MLSB_WORKING;
+  c.maxit = 0;
+  return c;
+}
+
+int mlsb_lse_direct(const double* A, int64_t lda, const double* B, int64_t ldb, const double* b,
+                    const double* d, int64_t m, int64_t n, int64_t p, double* x, double* r,
+                    double* v, int64_t* singular_index, const mlsb_exec* exec) {
+  if (m <= 0 || n <= 0 || p <= 0) return fail(MLSB_ERR_DIMENSION, "lse_problem: empty matrix");
+  if (p > n || n > m + p)
+    return fail(MLSB_ERR_DIMENSION, "lse_problem: requires p <= n <= m + p");
+  if (lda < m || ldb < p) return fail(MLSB_ERR_DIMENSION, "lse_problem: leading dimension too small");
+  if (!A || !B || !b || !d) return fail(MLSB_ERR_DIMENSION, "lse_problem: null input");
+  const mlsb_config c = direct_config();
+  return solve_single(lse_shape(m, n, p), A, lda, B, ldb, b, d, &c, x, r, v, nullptr,
+                      singular_index, exec);
+}
+
+int mlsb_gls_direct(const double* W, int64_t ldw, const double* V, int64_t ldv, const double* d,
+                    int64_t n, int64_t m, int64_t p, double* x, double* y, double* z,
+                    int64_t* singular_index, const mlsb_exec* exec) {
+  if (n <= 0 || m <= 0 || p <= 0) return fail(MLSB_ERR_DIMENSION, "gls_problem: empty matrix");
+  if (m > n || n > m + p) return fail(MLSB_ERR_DIMENSION, "gls_problem: requires m <= n <= m + p");
+  if (ldw < n || ldv < n) return fail(MLSB_ERR_DIMENSION, "gls_problem: leading dimension too small");
+  if (!W || !V || !d) return fail(MLSB_ERR_DIMENSION, "gls_problem: null input");
+  const mlsb_config c = direct_config();
+  return solve_single(gls_shape(n, m, p), W, ldw, V, ldv, nullptr, d, &c, x, y, z, nullptr,
+                      singular_index, exec);
+}
+
 int mlsb_mplse_z(const double* A, int64_t lda, const double* B, int64_t ldb, const double* b,
                  const double* d, int64_t m, int64_t n, int64_t p, const mlsb_config* cfg,
                  double* x, double* r, double* v, mlsb_trace* trace, int64_t* singular_index,

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 
+#include "mixedls/experiment.hpp"
 #include "mixedls/generate.hpp"
 #include "mixedls/gls.hpp"
 #include "mixedls/lse.hpp"
@@ -50,6 +51,10 @@ int main() {
               refg.trace.iterations, gpug.trace.iterations, to_string(refg.trace.status),
               to_string(gpug.trace.status), reldiff(gpug.state.x, refg.state.x),
               reldiff(gpug.state.y, refg.state.y));
+  // binary64 direct reference (experiment harness err-2 denominator)
+  auto dref = detail::lse_direct_reference(pb).state;
+  auto dgpu = b200::lse_direct_reference(pb);
+  std::printf("DIRECT relx %.3e relr %.3e\n", reldiff(dgpu.x, dref.x), reldiff(dgpu.r, dref.r));
   // exception parity: the reference's validation is reused verbatim
   lse_problem bad = pb;
   bad.d.pop_back();

@@ -24,6 +24,8 @@ def test_reference_program_through_shim(gpu):
     assert abs(int(gls[1]) - int(gls[2])) <= 1 and gls[3] == gls[4] == "converged"
     assert float(gls[5]) <= 1e-9 and float(gls[6]) <= 1e-9
     assert "EXC dimension_error" in out
+    dr = re.search(r"DIRECT relx (\S+) relr (\S+)", out)
+    assert dr and float(dr[1]) <= 1e-9 and float(dr[2]) <= 1e-9, out
 
 
 def test_dropin_demo_exception_path_without_gpu():

@@ -226,8 +226,112 @@ int solve_large(const Shape& s, int esz, const void* A, int64_t lda, const void*
   return MLSB_OK;
 }
 
-// Run `batch` problems.  Host mode: copy in, solve, copy out, synchronize.
-// Device mode: launch only (asynchronous on the stream).
+int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA, const double* B,
+        int64_t ldb, int64_t sB, const double* b, int64_t sb, const double* d, int64_t sd,
+        const mlsb_config* cfg, double* x, double* r, double* v, int32_t* status, int64_t* iters,
+        int32_t* errcode, int64_t* sing, double* hist, double* phases_out, bool force_sync,
+        const mlsb_exec* ex);
+
+// Host-buffer batches: chunks of problems flow through NSLOT device slots on
+// NSLOT streams, so the host->device copy of chunk k+1 (the bound: 295 KB per
+// C4 problem over PCIe) overlaps the solve of chunk k and the copy-back of
+// chunk k-1.  Each chunk is a device-mode launch of the same solver.
+constexpr int64_t kChunk = 4096;
+constexpr int NSLOT = 3;
+int run_pipelined(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
+                  const double* B, int64_t ldb, int64_t sB, const double* b, int64_t sb,
+                  const double* d, int64_t sd, const mlsb_config* cfg, double* x, double* r,
+                  double* v, int32_t* status, int64_t* iters, int32_t* errcode, int64_t* sing,
+                  double* hist, const mlsb_exec* ex) {
+  cudaStream_t user = ex ? static_cast<cudaStream_t>(ex->stream) : nullptr;
+  const int64_t spanA = (kChunk - 1) * sA + lda * (s.ca - 1) + s.ra;
+  const int64_t spanB = (kChunk - 1) * sB + ldb * (s.cb - 1) + s.rb;
+  const int64_t spanb = s.nb > 0 ? (kChunk - 1) * sb + s.nb : 0;
+  const int64_t spand = (kChunk - 1) * sd + s.nd;
+  const int64_t nh = hist ? cfg->maxit * 3 : 0;
+  struct Slot {
+    cudaStream_t st = nullptr;
+    DevBuf A, B, b, d, x, r, v, status, iters, err, sing, hist;
+  } slot[NSLOT];
+  cudaError_t e = cudaSuccess;
+  cudaEvent_t start;
+  if ((e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming))) return cuda_fail(e, "event");
+  cudaEventRecord(start, user);  // chunks start after the caller's prior work
+  int rc = MLSB_OK;
+  for (int k = 0; k < NSLOT && !e; ++k) {
+    Slot& S = slot[k];
+    if ((e = cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking))) break;
+    cudaStreamWaitEvent(S.st, start, 0);
+    if ((e = S.A.alloc(8 * spanA, S.st)) || (e = S.B.alloc(8 * spanB, S.st)) ||
+        (e = S.b.alloc(8 * (spanb + 1), S.st)) || (e = S.d.alloc(8 * spand, S.st)) ||
+        (e = S.x.alloc(8 * kChunk * s.nx, S.st)) || (e = S.r.alloc(8 * kChunk * s.nr, S.st)) ||
+        (e = S.v.alloc(8 * kChunk * s.nv, S.st)) || (e = S.status.alloc(4 * kChunk, S.st)) ||
+        (e = S.iters.alloc(8 * kChunk, S.st)) || (e = S.err.alloc(4 * kChunk, S.st)) ||
+        (e = S.sing.alloc(8 * kChunk, S.st)) || (e = S.hist.alloc(8 * kChunk * (nh + 1), S.st)))
+      break;
+  }
+  for (int64_t c0 = 0, k = 0; c0 < batch && !e && rc == MLSB_OK; c0 += kChunk, ++k) {
+    Slot& S = slot[k % NSLOT];
+    const int64_t nb = std::min<int64_t>(kChunk, batch - c0);
+    const int64_t nA = (nb - 1) * sA + lda * (s.ca - 1) + s.ra;
+    const int64_t nB = (nb - 1) * sB + ldb * (s.cb - 1) + s.rb;
+    const int64_t nd = (nb - 1) * sd + s.nd;
+    if ((e = cudaMemcpyAsync(S.A.p, A + c0 * sA, 8 * nA, cudaMemcpyHostToDevice, S.st)) ||
+        (e = cudaMemcpyAsync(S.B.p, B + c0 * sB, 8 * nB, cudaMemcpyHostToDevice, S.st)) ||
+        (e = cudaMemcpyAsync(S.d.p, d + c0 * sd, 8 * nd, cudaMemcpyHostToDevice, S.st)))
+      break;
+    if (s.nb > 0 && (e = cudaMemcpyAsync(S.b.p, b + c0 * sb, 8 * ((nb - 1) * sb + s.nb),
+                                         cudaMemcpyHostToDevice, S.st)))
+      break;
+    const mlsb_exec dex{MLSB_DEVICE, ex ? ex->device : -1, S.st};
+    rc = run(s, nb, S.A.as<double>(), lda, sA, S.B.as<double>(), ldb, sB,
+             s.nb > 0 ? S.b.as<double>() : nullptr, sb, S.d.as<double>(), sd, cfg, S.x.as<double>(),
+             S.r.as<double>(), S.v.as<double>(), S.status.as<int32_t>(), S.iters.as<int64_t>(),
+             S.err.as<int32_t>(), S.sing.as<int64_t>(), hist ? S.hist.as<double>() : nullptr,
+             nullptr, false, &dex);
+    if (rc) break;
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, S.st) : cudaSuccess;
+    };
+    if ((e = d2h(x ? x + c0 * s.nx : nullptr, S.x.p, 8 * nb * s.nx)) ||
+        (e = d2h(r ? r + c0 * s.nr : nullptr, S.r.p, 8 * nb * s.nr)) ||
+        (e = d2h(v ? v + c0 * s.nv : nullptr, S.v.p, 8 * nb * s.nv)) ||
+        (e = d2h(status ? status + c0 : nullptr, S.status.p, 4 * nb)) ||
+        (e = d2h(iters ? iters + c0 : nullptr, S.iters.p, 8 * nb)) ||
+        (e = d2h(errcode ? errcode + c0 : nullptr, S.err.p, 4 * nb)) ||
+        (e = d2h(sing ? sing + c0 : nullptr, S.sing.p, 8 * nb)) ||
+        (e = d2h(hist ? hist + c0 * nh : nullptr, S.hist.p, 8 * nb * nh)))
+      break;
+  }
+  cudaError_t es = cudaSuccess;
+  for (int k = 0; k < NSLOT; ++k)
+    if (slot[k].st) {
+      const cudaError_t ek = cudaStreamSynchronize(slot[k].st);
+      if (ek && !es) es = ek;
+    }
+  for (int k = NSLOT - 1; k >= 0; --k) {  // buffers are freed (stream-ordered) before the streams
+    Slot& S = slot[k];
+    for (DevBuf* bf : {&S.A, &S.B, &S.b, &S.d, &S.x, &S.r, &S.v, &S.status, &S.iters, &S.err,
+                       &S.sing, &S.hist})
+      if (bf->p) {
+        cudaFreeAsync(bf->p, S.st);
+        bf->p = nullptr;
+      }
+    if (S.st) {
+      cudaStreamSynchronize(S.st);
+      cudaStreamDestroy(S.st);
+    }
+  }
+  cudaEventDestroy(start);
+  if (rc) return rc;
+  if (e) return cuda_fail(e, "pipelined batch");
+  if (es) return cuda_fail(es, "pipelined batch: cudaStreamSynchronize");
+  return MLSB_OK;
+}
+
+// Run `batch` problems.  Host mode: copy in, solve, copy out, synchronize
+// (large host batches go through run_pipelined).  Device mode: launch only
+// (asynchronous on the stream).
 int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA, const double* B,
         int64_t ldb, int64_t sB, const double* b, int64_t sb, const double* d, int64_t sd,
         const mlsb_config* cfg, double* x, double* r, double* v, int32_t* status, int64_t* iters,
@@ -261,6 +365,9 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
     if (dev) cudaStreamSynchronize(st);
     return MLSB_OK;
   }
+  if (!dev && !phases_out && batch >= 2 * kChunk && !getenv("MLSB_DEBUG_STAMPS"))
+    return run_pipelined(s, batch, A, lda, sA, B, ldb, sB, b, sb, d, sd, cfg, x, r, v, status, iters,
+                         errcode, sing, hist, ex);
   const bool use_reg = s.kind == mlsb::KIND_LSE &&
                        mlsb::lse_reg_supported(s.m, s.n, s.p, cfg->u_f, cfg->u_s, cfg->u_r, lim);
   // factors in shared memory when they fit, else in an L2-resident global workspace

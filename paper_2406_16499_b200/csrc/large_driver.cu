@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "large_common.cuh"
@@ -421,6 +422,8 @@ static cudaError_t rq_stage(FT* M, int64_t ld, int rb, int rr, int cb, int cc, F
 template <class FT, class WT, class CT>
 static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   const bool lse = P.kind == KIND_LSE;
+  constexpr bool kReal = std::is_same<WT, double>::value;
+  const bool ext = kReal && P.u_r == 2;
   const int m = int(P.m), n = int(P.n), p = int(P.p);
   const int R = lse ? m + p : n, C = lse ? n : m + p;
   const int64_t ld = R;
@@ -437,6 +440,7 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
                                      size_t(nbz + nbq) * NB * NB + size_t(C + R) + 2 * size_t(R) * NB +
                                      wn + 8 * size_t(L)) +
                        sizeof(WT) * (size_t(R) * (6 + ntc) + size_t(C) * (5 + ntr)) +
+                       (ext ? 16 * (size_t(ntc) * R + size_t(ntr) * C) + 8 * size_t(R) : 0) +
                        sizeof(CT) * (10 * size_t(L) + 32 * 256) + 64 * 1024 + 64 * 256;
   cudaError_t e = ar.init(bytes + bytes / 4 + (1 << 20), st);
   if (e) return MLSB_ERR_CUDA;
@@ -463,6 +467,11 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   WT* rpart = ar.take<WT>(size_t(ntc) * R);
   WT* cpart = ar.take<WT>(size_t(ntr) * C);
   WT* gvec = ar.take<WT>(C);
+  // u_r = extended (real only): double-double tile partials and the low
+  // words of the row initialisers
+  double2* rpartX = ext ? ar.take<double2>(size_t(ntc) * R) : nullptr;
+  double2* cpartX = ext ? ar.take<double2>(size_t(ntr) * C) : nullptr;
+  double* rlo = ext ? ar.take<double>(R) : nullptr;
   CT* cv[10];
   for (int i = 0; i < 10; ++i) cv[i] = ar.take<CT>(L);
   CT* ypart = ar.take<CT>(32 * 256);
@@ -620,9 +629,20 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       Stack<WT> S{gA, gB, P.lda, P.ldb, m, true, 1.0 / sA, 1.0 / sB};
       k_fill<WT><<<nblk(n), KT, 0, st>>>(gvec, n, zero<WT>());
       dim3 g2((m + RTR - 1) / RTR, ntc);
-      k_resid_tile<WT><<<g2, KT, 0, st>>>(S, m, n, gvec, sw, rpart, cpart);
-      k_resid_reduce<WT><<<nblk(m + n), KT, 0, st>>>(m, n, ntc, (m + RTR - 1) / RTR, rpart, cpart, rinit,
-                                                     nullptr, rout, cout);
+      if constexpr (kReal) {
+        if (ext) {  // g = A^T r accumulated in double-double (gemv_extended, matrix.hpp:157-170)
+          const StackX SX{gA, gB, P.lda, P.ldb, m, true, sA, sB};
+          k_resid_tile_dd<<<g2, KT, 0, st>>>(SX, m, n, gvec, sw, rpartX, cpartX);
+          k_resid_reduce_dd<<<nblk(m + n), KT, 0, st>>>(m, n, ntc, (m + RTR - 1) / RTR, rpartX,
+                                                         cpartX, nullptr, nullptr, nullptr, nullptr,
+                                                         cout);
+        }
+      }
+      if (!ext) {
+        k_resid_tile<WT><<<g2, KT, 0, st>>>(S, m, n, gvec, sw, rpart, cpart);
+        k_resid_reduce<WT><<<nblk(m + n), KT, 0, st>>>(m, n, ntc, (m + RTR - 1) / RTR, rpart, cpart,
+                                                       rinit, nullptr, rout, cout);
+      }
       cudaMemsetAsync(bits + 4, 0, 8, st);
       k_vmax<WT><<<nblk(n), KT, 0, st>>>(cout, n, bits + 4);
       k_demote<WT, FT><<<nblk(n), KT, 0, st>>>(cout, n, bits + 4, gf);
@@ -680,8 +700,25 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       k_neg<WT><<<nblk(p), KT, 0, st>>>(cinit + m, p);                          // [0; -y]
     }
     dim3 g2(ntr, ntc);
-    k_resid_tile<WT><<<g2, KT, 0, st>>>(S, R, C, su, wvec, rpart, cpart);
-    k_resid_reduce<WT><<<nblk(R + C), KT, 0, st>>>(R, C, ntc, ntr, rpart, cpart, rrow, cinit, rout, cout);
+    if constexpr (kReal) {
+      if (ext) {  // lse.hpp:200-257 / gls.hpp:178-231
+        if (lse) {
+          k_sub_dd<<<nblk(m), KT, 0, st>>>(rinit, sw, m, rrow, rlo);  // TwoSum(b, -r)
+          k_fill<double><<<nblk(p), KT, 0, st>>>(rlo + m, p, 0.0);
+        } else {
+          k_fill<double><<<nblk(n), KT, 0, st>>>(rlo, n, 0.0);
+        }
+        const StackX SX{gA, gB, P.lda, P.ldb, m, lse, sA, sB};
+        k_resid_tile_dd<<<g2, KT, 0, st>>>(SX, R, C, su, wvec, rpartX, cpartX);
+        k_resid_reduce_dd<<<nblk(R + C), KT, 0, st>>>(R, C, ntc, ntr, rpartX, cpartX, rrow, rlo, cinit,
+                                                      rout, cout);
+      }
+    }
+    if (!ext) {
+      k_resid_tile<WT><<<g2, KT, 0, st>>>(S, R, C, su, wvec, rpart, cpart);
+      k_resid_reduce<WT><<<nblk(R + C), KT, 0, st>>>(R, C, ntc, ntr, rpart, cpart, rrow, cinit, rout,
+                                                     cout);
+    }
     StopIn si{};
     if (lse) {  // f1, f2, f3 | r, v, x
       si.seg[0] = rout;       si.len[0] = m;
@@ -850,7 +887,9 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
 }
 
 int large_solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
-  if (P.u_f != 0 || P.u_r == 2) return MLSB_ERR_UNSUPPORTED;
+  // u_f = working needs binary64 WY GEMMs and panels (not built yet); the
+  // extended residual is real-only (the reference has no complex path)
+  if (P.u_f != 0 || (P.u_r == 2 && P.cplx)) return MLSB_ERR_UNSUPPORTED;
   if (P.cplx) {
     if (P.u_s != 0) return solve<cf, cd, cd>(P, st, out);
     return solve<cf, cd, cf>(P, st, out);

@@ -122,3 +122,49 @@ def test_large_determinism(gpu):
     r2 = P.mplse(P.LseProblem(A, B, b, d))
     assert np.array_equal(r1.state.x, r2.state.x)
     assert np.array_equal(r1.trace.residual_history, r2.trace.residual_history)
+
+
+# u_r = extended (double-double residuals, lse.hpp:200-257 / gls.hpp:178-231) on the large path
+def _cfg_ext(P, maxit=40):
+    return P.RefinementConfig(maxit=maxit, precisions=P.PrecisionConfig("low", "low", "working",
+                                                                        "extended"))
+
+
+@pytest.mark.parametrize("shape", [(20, 10, 4), (70, 40, 33), (100, 64, 64)])
+def test_lse_large_path_extended(gpu, port, force_large, shape):
+    m, n, p = shape
+    A, B, b, d = G.lse_problem(m, n, p, 1e4, 1e2, seed=m + 2 * n + p)
+    res = gpu.mplse(gpu.LseProblem(A, B, b, d), _cfg_ext(gpu))
+    ref = port.mplse(A, B, b, d, prec=("s", "s", "dd"))
+    kappa = np.linalg.cond(np.vstack([A, B])) * 1e2
+    msgs = check_parity("lse", rel(res.state.x, ref.x), fwd_bound(m, n, p, kappa),
+                        res.trace.iterations, ref.iterations,
+                        lse_backward(A, B, b, d, res.state.x, res.state.r, res.state.v),
+                        lse_backward(A, B, b, d, ref.x, ref.r, ref.v), res.trace.status, ref.status)
+    assert res.trace.status == ref.status
+    assert not msgs, msgs
+
+
+@pytest.mark.parametrize("shape", [(40, 20, 30), (64, 33, 40)])
+def test_gls_large_path_extended(gpu, port, force_large, shape):
+    n, m, p = shape
+    W, V, d = G.gls_problem(n, m, p, 1e4, 1e2, seed=n + 2 * m + p)
+    res = gpu.mpgls(gpu.GlsProblem(W, V, d), _cfg_ext(gpu))
+    ref = port.mpgls(W, V, d, prec=("s", "s", "dd"))
+    kappa = np.linalg.cond(np.hstack([W, V])) * 1e2
+    fwd = max(rel(res.state.x, ref.x), rel(res.state.y, ref.r))
+    msgs = check_parity("gls", fwd, fwd_bound(m, n, p, kappa), res.trace.iterations, ref.iterations,
+                        gls_backward(W, V, d, res.state.x, res.state.y, res.state.z),
+                        gls_backward(W, V, d, ref.x, ref.r, ref.v), res.trace.status, ref.status)
+    assert res.trace.status == ref.status
+    assert not msgs, msgs
+
+
+def test_lse_large_size_extended(gpu, port):
+    """A size the large path takes on its own, u_r = extended."""
+    A, B, b, d = G.lse_problem(1024, 512, 128, 1e5, 1e2, seed=4)
+    res = gpu.mplse(gpu.LseProblem(A, B, b, d), _cfg_ext(gpu))
+    ref = port.mplse(A, B, b, d, prec=("s", "s", "dd"))
+    assert res.trace.status == ref.status == "converged"
+    assert abs(res.trace.iterations - ref.iterations) <= 1
+    assert rel(res.state.x, ref.x) <= fwd_bound(1024, 512, 128, 1e5 * 10)

@@ -416,19 +416,27 @@ __device__ void build_T(float* G, const float* tau, int kb, int l) {
 
 // xLARFG (householder.hpp:30-53) from alpha and a2ss = alpha^2 + ||x||^2.
 // beta, tau and 1/(alpha - beta) -- which the reference rounds to binary32
-// anyway -- come from correctly rounded binary32 sqrt and reciprocals, which
-// keeps the long-latency binary64 operations off the critical path of every
-// reflector step (a few ulps of u_f, well inside the factorization error).
+// anyway -- come from the hardware rsqrt / rcp refined by one Newton step
+// (<= 1 ulp, no slow-path branches), which keeps the long-latency binary64
+// operations off the critical path of every reflector step (a few ulps of
+// u_f, well inside the factorization error).
 __device__ __forceinline__ void larfg(float alpha, bool nonzero, float a2ss, float& tj, float& inv,
                                       float& beta) {
   tj = 0.f;
   inv = 1.f;
   beta = alpha;
   if (nonzero) {
-    const float bt = -copysignf(__fsqrt_rn(a2ss), alpha);
-    const float rb = __frcp_rn(bt);
-    inv = __frcp_rn(__fsub_rn(alpha, bt));
-    tj = __fmul_rn(__fsub_rn(bt, alpha), rb);
+    // hardware rsqrt/rcp + one Newton step each (<= 1 ulp, no slow-path branches)
+    const float rs = rsqrtf(a2ss);
+    float nrm = a2ss * rs;
+    nrm = fmaf(fmaf(-nrm, nrm, a2ss), 0.5f * rs, nrm);
+    const float bt = -copysignf(nrm, alpha);
+    const float db = alpha - bt;
+    float rb = __fdividef(1.f, bt), ri = __fdividef(1.f, db);
+    rb = fmaf(rb, fmaf(-bt, rb, 1.f), rb);
+    ri = fmaf(ri, fmaf(-db, ri, 1.f), ri);
+    tj = (bt - alpha) * rb;
+    inv = ri;
     beta = bt;
   }
 }

@@ -498,7 +498,7 @@ __device__ __forceinline__ Col9 gen_col_core(Col9 col, int jc, int t0, int m, in
     if (t < t0) {
       val = 0.f;
     } else if (i > jc && i < m) {
-      if (tj != 0.f) val *= inv;
+      val *= inv;  // inv = 1 when tau = 0
       col.v[t] = val;
     } else {
       val = (i == jc) ? 1.f : 0.f;
@@ -522,6 +522,7 @@ __device__ __forceinline__ void gen_col(float (&ar)[RT][CS], int jc, int m, int 
 
 // RQ layout: lane l <-> columns l + 32 s (s < BS), warp w <-> rows w + 16 t (t < BT)
 constexpr int BT = 18, BS = 4;
+static_assert(BS == 4, "rq_crit's dot is written for 4 column slots");
 
 // RQ reflector of row m+j held by its owner warp (lane l holds columns
 // l + 32 s): x = row[c < pc], alpha = row[pc]; v published with the unit at pc
@@ -544,7 +545,7 @@ __device__ __forceinline__ Row4 gen_row_core(Row4 row, int j, int pc, int C, int
     const int c = l + 32 * s;
     float val = row.v[s];
     if (c < pc) {
-      if (tj != 0.f) val *= inv;
+      val *= inv;  // inv = 1 when tau = 0
       row.v[s] = val;
     } else {
       if (c == pc) row.v[s] = beta;
@@ -634,10 +635,8 @@ __device__ __forceinline__ void rq_crit(float (&br)[BT][BS], const float (&vv)[B
                                         uint64_t* full, uint64_t* empty, int kn) {
   const int b = kn % NVB;
   if (kn >= NVB) mbar_wait(empty + b, ((kn / NVB) - 1) & 1);  // (long satisfied: off the chain)
-  float dc = 0.f;
-#pragma unroll
-  for (int s = 0; s < BS; ++s) dc = fmaf(br[TO][s], vv[s], dc);
-  dc = warp_sum(dc);
+  const float dc = warp_sum(fmaf(br[TO][0], vv[0], br[TO][1] * vv[1]) +
+                           fmaf(br[TO][2], vv[2], br[TO][3] * vv[3]));
   if (tj != 0.f)
 #pragma unroll
     for (int s = 0; s < BS; ++s) br[TO][s] = fmaf(-(tj * vv[s]), dc, br[TO][s]);

@@ -479,12 +479,12 @@ __device__ __forceinline__ void tail_norm(const float (&v)[K], const Pred& live,
 struct Col9 {
   float v[RT];
 };
-__device__ __forceinline__ Col9 gen_col_core(Col9 col, int jc, int t0, int m, int l, float* vout,
+template <int t0>
+__device__ __forceinline__ Col9 gen_col_core(Col9 col, int jc, int m, int l, float* vout,
                                           float* tau1) {
-  float a9 = 0.f;
-#pragma unroll
-  for (int t = 0; t < RT; ++t) a9 = (t == (jc >> 5)) ? col.v[t] : a9;
-  const float alpha = __shfl_sync(0xffffffffu, a9, jc & 31);
+  // the pivot row jc = 16 SC + w of column slot SC lives in row slot SC / 2 = t0:
+  // a static index (a runtime-indexed pick would put the column in local memory)
+  const float alpha = __shfl_sync(0xffffffffu, col.v[t0 < RT ? t0 : RT - 1], jc & 31);
   bool nz;
   float a2ss;
   tail_norm(col.v, [&](int t) { const int i = l + 32 * t; return t >= t0 && i > jc && i < m; },
@@ -515,7 +515,7 @@ __device__ __forceinline__ void gen_col(float (&ar)[RT][CS], int jc, int m, int 
   Col9 c;
 #pragma unroll
   for (int t = 0; t < RT; ++t) c.v[t] = ar[t][SC];
-  c = gen_col_core(c, jc, SC / 2, m, l, vout, tau1);
+  c = gen_col_core<SC / 2>(c, jc, m, l, vout, tau1);
 #pragma unroll
   for (int t = 0; t < RT; ++t) ar[t][SC] = c.v[t];
 }
@@ -531,10 +531,14 @@ struct Row4 {
 };
 __device__ __forceinline__ Row4 gen_row_core(Row4 row, int j, int pc, int C, int l, float* vout,
                                           float* tau2) {
-  float a4 = 0.f;
+  // pivot column pc: shuffle every column slot, then pick (a runtime-indexed
+  // pick of row.v would put the row in local memory)
+  float alpha = 0.f;
 #pragma unroll
-  for (int s = 0; s < BS; ++s) a4 = (s == (pc >> 5)) ? row.v[s] : a4;
-  const float alpha = __shfl_sync(0xffffffffu, a4, pc & 31);
+  for (int s = 0; s < BS; ++s) {
+    const float a = __shfl_sync(0xffffffffu, row.v[s], pc & 31);
+    alpha = (s == (pc >> 5)) ? a : alpha;
+  }
   bool nz;
   float a2ss;
   tail_norm(row.v, [&](int s) { return l + 32 * s < pc; }, alpha, nz, a2ss);
@@ -621,7 +625,7 @@ constexpr int NVB = 4;
 
 #ifdef MLSB_PROBE
 // debug: clock64 stamps of problem 0 inside QR steps 40/41 (slots 64..127)
-__device__ unsigned long long* g_probe = nullptr;
+__constant__ unsigned long long* g_probe = nullptr;
 #define PROBE(k) do { if (g_probe && blockIdx.x == 0) g_probe[k] = clock64(); } while (0)
 #else
 #define PROBE(k) do { } while (0)

@@ -525,6 +525,10 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
     if (void* pp = probe) {
       unsigned long long pr[128];
       cudaMemcpy(pr, pp, sizeof(pr), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "MLSB_PROBE raw (cycles from slot 0):");
+      for (int i = 0; i < 40; ++i)
+        if (pr[i]) fprintf(stderr, " [%d] %lld", i, (long long)(pr[i] - pr[0]));
+      fprintf(stderr, "\n");
       fprintf(stderr, "MLSB_PROBE per QR step j1 (owner warp): sum/upd/gen/pub cycles after previous publish\n");
       for (int i = 1; i < 32; ++i)
         if (pr[i] && pr[96 + i - 1])

@@ -116,6 +116,20 @@ __device__ __forceinline__ void reduce_live(float (&d)[8], int l) {
     if (S0 + q < 8) d[S0 + q] = __shfl_sync(0xffffffffu, mine, q << (5 - K));
 }
 
+#ifdef MLSB_PROBE
+// debug: clock64 stamps of problem 0 inside QR steps 40/41 (slots 64..127)
+__constant__ unsigned long long* g_probe = nullptr;
+#define PROBE(k) do { if (g_probe && blockIdx.x == 0) g_probe[k] = clock64(); } while (0)
+#else
+#define PROBE(k) do { } while (0)
+#endif
+#ifdef MLSB_PROBE_WY
+// first-occurrence stamps (warp 0 of the group, problem 0)
+#define PROBE1(k) do { if (g_probe && blockIdx.x == 0) g_probe[k] = clock64(); } while (0)
+#else
+#define PROBE1(k) do { } while (0)
+#endif
+
 // ------------------------------------------- multi-warp WY block applies
 // T blocks (32 x 32, forward xLARFT) use a padded column stride so that both
 // row and column walks by a warp are bank-conflict free.
@@ -170,9 +184,11 @@ __device__ __forceinline__ CT tsum32(const float (&v)[32], CT xv, int l) {
 // double-buffered by the caller, so one barrier per block).
 template <class CT, class VF>
 __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, const float* Tb,
-                                         bool tr, CT* x, CT* part, const Grp& g) {
+                                         bool tr, CT* x, CT* part, CT* ws, const Grp& g) {
   const int l = g.l, i = 32 * g.gw + l;
   const bool act = i >= i0 && i < i1;
+  const int pk = (g.gw == 0 && l == 0 && tr) ? 8 * (i0 >> 5) : -1;
+  if (pk >= 0) PROBE1(pk);
   float v[32];
 #pragma unroll
   for (int q = 0; q < 32; ++q) {
@@ -181,14 +197,19 @@ __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, c
   }
   const CT xi = act ? x[i] : CT(0);
   part[32 * g.gw + l] = tsum32(v, xi, l);
+  if (pk >= 0) PROBE1(pk + 1);
   g.sync();
+  if (pk >= 0) PROBE1(pk + 2);
   CT y = CT(0);
   for (int w2 = 0; w2 < g.ngw; ++w2) y += part[32 * w2 + l];
-  // z = T' y, lane l -> z_l
+  // z = T' y, lane l -> z_l; y and z go through the warp's shared scratch `ws`
+  // (broadcast reads that issue ahead, instead of a shuffle per term)
+  ws[l] = y;
+  __syncwarp();
   CT z0 = CT(0), z1 = CT(0);
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
-    const CT yk = __shfl_sync(0xffffffffu, y, k);
+    const CT yk = ws[k];
     const bool use = k < kb && (tr ? k <= l : k >= l);
     const float tv = Tb[tr ? k + TLD * l : l + TLD * k];
     const float t = use ? tv : 0.f;
@@ -196,13 +217,19 @@ __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, c
     else z0 += CT(t) * yk;
   }
   const CT z = l < kb ? z0 + z1 : CT(0);
+  if (pk >= 0) PROBE1(pk + 3);
+  __syncwarp();
+  ws[l] = z;
+  __syncwarp();
   CT a0 = CT(0), a1 = CT(0);
 #pragma unroll
   for (int q = 0; q < 32; q += 2) {
-    a0 += CT(v[q]) * __shfl_sync(0xffffffffu, z, q);
-    a1 += CT(v[q + 1]) * __shfl_sync(0xffffffffu, z, q + 1);
+    a0 += CT(v[q]) * ws[q];
+    a1 += CT(v[q + 1]) * ws[q + 1];
   }
+  __syncwarp();  // ws is rewritten by the next block
   if (act) x[i] = xi - (a0 + a1);
+  if (pk >= 0) PROBE1(pk + 4);
 }
 
 // QR (Z) reflectors: v_q = e_{j0+q} + M[j0+q+1 : rend, j0+q]; entry index = row
@@ -211,8 +238,10 @@ struct ZV {
   int ld, j0, rmax, cmax;  // clamps keep the (unconditional) load inside M
   __device__ __forceinline__ float operator()(int r, int q) const {
     const int d = r - j0;
-    const int rr = r < rmax ? r : rmax, cc = j0 + q < cmax ? j0 + q : cmax;
-    const float mv = M[rr + size_t(cc) * ld];
+    // rows clamped; columns past the last reflector stay inside the shared
+    // allocation (masked by the caller)
+    const int rr = r < rmax ? r : rmax;
+    const float mv = M[rr + size_t(j0 + q) * ld];
     return d > q ? mv : (d == q ? 1.f : 0.f);
   }
 };
@@ -223,8 +252,8 @@ struct QV {
   int ld, row0, pc0, rmax, cmax;  // row0 = rtop + j0, pc0 = ptop + j0; load clamps
   __device__ __forceinline__ float operator()(int c, int q) const {
     const int pc = pc0 + q;
-    const int rr = row0 + q < rmax ? row0 + q : rmax, cc = c < cmax ? c : cmax;
-    const float mv = M[rr + size_t(cc) * ld];
+    const int cc = c < cmax ? c : cmax;  // rows past the last reflector stay inside M
+    const float mv = M[(row0 + q) + size_t(cc) * ld];
     return c < pc ? mv : (c == pc ? 1.f : 0.f);
   }
 };
@@ -234,27 +263,27 @@ struct QV {
 // separated by a barrier (the part buffers restart at 0).
 template <class CT>
 __device__ void z_apply_mw(const float* M, int ld, int k, int rend, const float* TZ, bool herm,
-                           CT* x, CT* part, const Grp& g) {
+                           CT* x, CT* part, CT* ws, const Grp& g) {
   const int nb = (k + 31) / 32;
   for (int s = 0; s < nb; ++s) {
     const int b = herm ? s : nb - 1 - s;
     const int j0 = 32 * b, kb = (k - j0) < 32 ? (k - j0) : 32;
     wy_block(ZV{M, ld, j0, ld - 1, k - 1}, j0, rend, kb, TZ + b * TSZ, herm, x,
-             part + (s & 1) * 32 * g.ngw, g);
+             part + (s & 1) * 32 * g.ngw, ws, g);
   }
 }
 
 // Q x / Q^T x over the first dim entries; group of >= ceil(dim / 32) warps
 template <class CT>
 __device__ void q_apply_mw(const float* M, int ld, int kq, int rtop, int ptop, int dim,
-                           const float* TQ, bool herm, CT* x, CT* part, const Grp& g) {
+                           const float* TQ, bool herm, CT* x, CT* part, CT* ws, const Grp& g) {
   const int nb = (kq + 31) / 32;
   for (int s = 0; s < nb; ++s) {
     const int b = herm ? s : nb - 1 - s;
     const int j0 = 32 * b, kb = (kq - j0) < 32 ? (kq - j0) : 32;
     const int cmax = (ptop + j0 + kb) < dim ? (ptop + j0 + kb) : dim;
     wy_block(QV{M, ld, rtop + j0, ptop + j0, rtop + kq - 1, dim - 1}, 0, cmax, kb, TQ + b * TSZ,
-             herm, x, part + (s & 1) * 32 * g.ngw, g);
+             herm, x, part + (s & 1) * 32 * g.ngw, ws, g);
   }
 }
 
@@ -623,13 +652,6 @@ __device__ __forceinline__ void reduce16(float (&d)[16], int l) {
 // factorization).
 constexpr int NVB = 4;
 
-#ifdef MLSB_PROBE
-// debug: clock64 stamps of problem 0 inside QR steps 40/41 (slots 64..127)
-__constant__ unsigned long long* g_probe = nullptr;
-#define PROBE(k) do { if (g_probe && blockIdx.x == 0) g_probe[k] = clock64(); } while (0)
-#else
-#define PROBE(k) do { } while (0)
-#endif
 
 // RQ owner path: apply reflector (vv, tj) to the owner's row slot TO, then
 // generate the next reflector (index jn, pivot pc, sequence number kn) from it.
@@ -741,7 +763,11 @@ __device__ __forceinline__ void qr_crit(float (&ar)[RT][CS], const float (&vr)[R
   dc = warp_sum(dc);
   // probe layout (steps j1 = 33..64): [j1-33] warp_sum done, [32+..] update done,
   // [64+..] gen done, [96+..] published
+#ifdef MLSB_PROBE_WY
+  const int pb = -1;
+#else
   const int pb = (j1 >= 33 && j1 < 65 && l == 0) ? j1 - 33 : -1;
+#endif
   if (pb >= 0) PROBE(pb);
   if (tj != 0.f) {
     const float sc = tj * dc;
@@ -861,6 +887,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   constexpr int ZG = 9, QG = 4;  // warps of the Z group (rows <= 288) and Q group (cols <= 128)
   CT* partZ = reinterpret_cast<CT*>(smem + Ly.oU);
   CT* partQ = partZ + 2 * 32 * ZG;
+  CT* wsc = partQ + 2 * 32 * QG + 32 * w;  // this warp's 32-entry scratch
   double* red = reinterpret_cast<double*>(smem + Ly.oRed);
   double* scal = reinterpret_cast<double*>(smem + Ly.oScal);
   int* iflag = reinterpret_cast<int*>(scal + S_FLAG);
@@ -1093,6 +1120,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     float* gf = reinterpret_cast<float*>(WC(5));
     float* partZf = reinterpret_cast<float*>(smem + Ly.oU);
     float* partQf = partZf + 2 * 32 * ZG;
+    float* wscf = partQf + 2 * 32 * QG + 32 * w;
     for (int i = tid; i < m; i += NT) {
       bf[i] = float(rinit[i]);
       c[i] = bf[i];
@@ -1102,7 +1130,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     if (w == 0) {
       trsv_up<float>(M, ld, m, n - p, p, rinvRf, y2, l);
     } else if (w >= NW - ZG) {
-      z_apply_mw<float>(M, ld, kz, m, TZ, true, c, partZf, Grp{w - (NW - ZG), ZG, l, 1});  // c = Z^T b
+      z_apply_mw<float>(M, ld, kz, m, TZ, true, c, partZf, wscf, Grp{w - (NW - ZG), ZG, l, 1});  // c = Z^T b
     }
     __syncthreads();
     if (iflag[0]) goto finish;
@@ -1117,7 +1145,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
         trsv_up<float>(M, ld, 0, 0, k, rinvTf, y, l);
       }
       g.sync();
-      q_apply_mw<float>(M, ld, p, m, n - p, n, TQ, true, y, partQf, g);  // x = Q^T [y1; y2]
+      q_apply_mw<float>(M, ld, p, m, n - p, n, TQ, true, y, partQf, wscf, g);  // x = Q^T [y1; y2]
     }
     __syncthreads();
     if (iflag[0]) goto finish;
@@ -1197,7 +1225,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       for (int j = tid; j < n; j += NT) gf[j] = float(cout[j] / sg);
       __syncthreads();
       if (w < QG) {
-        q_apply_mw<float>(M, ld, p, m, n - p, n, TQ, false, gf, partQf, Grp{w, QG, l, 2});  // Q g
+        q_apply_mw<float>(M, ld, p, m, n - p, n, TQ, false, gf, partQf, wscf, Grp{w, QG, l, 2});  // Q g
         if (w == 0) trsv_upt<float>(M, ld, m, n - p, p, rinvRf, gf + (n - p), l);
       }
       __syncthreads();
@@ -1347,10 +1375,10 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       for (int i = tid; i < p; i += NT) y2[i] = CT(rout[m + i] / sig);
       __syncthreads();
       if (w < ZG) {
-        z_apply_mw<CT>(M, ld, kz, m, TZ, true, wv, partZ, Grp{w, ZG, l, 1});  // w = Z^T f1
+        z_apply_mw<CT>(M, ld, kz, m, TZ, true, wv, partZ, wsc, Grp{w, ZG, l, 1});  // w = Z^T f1
         if (pass == 1) stampw(16, 0);
       } else if (w < ZG + QG) {
-        q_apply_mw<CT>(M, ld, p, m, n - p, n, TQ, false, u, partQ, Grp{w - ZG, QG, l, 2});  // u = Q f3
+        q_apply_mw<CT>(M, ld, p, m, n - p, n, TQ, false, u, partQ, wsc, Grp{w - ZG, QG, l, 2});  // u = Q f3
         if (pass == 1) stampw(17, ZG);
       } else if (w == ZG + QG) {
         trsv_up<CT>(M, ld, m, n - p, p, rinvR, y2, l);
@@ -1388,7 +1416,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
         if (w == 0) trsv_up<CT>(M, ld, 0, 0, k, rinvT, y, l);
         if (pass == 1) stampw(19, 0);
         g.sync();
-        q_apply_mw<CT>(M, ld, p, m, n - p, n, TQ, true, y, partQ, g);  // dx = Q^T y
+        q_apply_mw<CT>(M, ld, p, m, n - p, n, TQ, true, y, partQ, wsc, g);  // dx = Q^T y
         if (pass == 1) stampw(20, 0);
       } else if (w < NW - ZG) {
         // s = T12^T q1 + (T22^T q2 - u2)  (q = wv)
@@ -1397,7 +1425,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
         gemv_cols<CT, true>(M, ld, k, m - k, k, p, wv + k, q1, QG, NG, w, l);
         if (pass == 1) stampw(21, QG);
       } else {
-        z_apply_mw<CT>(M, ld, kz, m, TZ, false, dr, partZ, Grp{w - (NW - ZG), ZG, l, 1});  // dr = Z q
+        z_apply_mw<CT>(M, ld, kz, m, TZ, false, dr, partZ, wsc, Grp{w - (NW - ZG), ZG, l, 1});  // dr = Z q
         if (pass == 1) stampw(22, NW - ZG);
       }
       __syncthreads();

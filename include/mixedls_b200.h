@@ -124,6 +124,21 @@ int mlsb_gls_direct(const double* W, int64_t ldw, const double* V, int64_t ldv, 
                     int64_t n, int64_t m, int64_t p, double* x, double* y, double* z,
                     int64_t* singular_index, const mlsb_exec* exec);
 
+/* GMRES-IR for LSE (gmres_refine_lse, inc/krylov.hpp:545-689): the outer
+ * loop of mplse with each correction system solved by full MGS-GMRES
+ * (binary64, rel_tol 1e-6) on the alpha-scaled augmented operator, alpha =
+ * alpha_scale * ||r0||, preconditioned by the binary32 GRQ factors widened to
+ * binary64.  precond: MLSB_PRECOND_LEFT (krylov.hpp:209-230, with the
+ * triangular cascade as initial guess) or MLSB_PRECOND_BD_SPLIT (two-sided,
+ * krylov.hpp:253-287).  Built for u_f = low and m >= n (the split
+ * preconditioner's first case); other inputs return MLSB_ERR_UNSUPPORTED.
+ * trace->inner_iterations = total GMRES iterations. */
+enum { MLSB_PRECOND_LEFT = 0, MLSB_PRECOND_BD_SPLIT = 1 };
+int mlsb_gmres_lse(const double* A, int64_t lda, const double* B, int64_t ldb, const double* b,
+                   const double* d, int64_t m, int64_t n, int64_t p, const mlsb_config* cfg,
+                   int precond, double alpha_scale, double* x, double* r, double* v,
+                   mlsb_trace* trace, int64_t* singular_index, const mlsb_exec* exec);
+
 /* Complex128 problems (interleaved re, im; same shapes and semantics with
  * Hermitian transposes), solved with complex64 factors at u_f = low.  The
  * reference is real-only; these serve BASELINE config 5. */

@@ -46,6 +46,7 @@ class OracleResult:
     iterations: int
     history: np.ndarray
     phases: np.ndarray = field(default_factory=lambda: np.zeros(6))
+    inner: int = 0  # GMRES iterations (gmres_lse)
 
 
 _dp = C.POINTER(C.c_double)
@@ -215,6 +216,32 @@ class Oracle:
         if rc:
             raise OracleError(rc, sing.value)
         return dy, dz, dx
+
+    def gmres_lse(self, A, B, b, d, tol=1e-13, maxit=40, prec=("s", "s", "d"), precond="bd_split",
+                  alpha_scale=1.0):
+        """gmres_refine_lse (krylov.hpp:545) -- reference build only."""
+        if not hasattr(self.lib, "orc_gmres_lse"):
+            raise OracleError(9)
+        m, n = A.shape
+        p = B.shape[0]
+        A, B = _f(A), _f(B)
+        b = np.ascontiguousarray(b, np.float64)
+        d = np.ascontiguousarray(d, np.float64)
+        x, r, v = np.zeros(n), np.zeros(m), np.zeros(p)
+        st, it, inner = C.c_int32(0), C.c_int64(0), C.c_int64(0)
+        hist = np.zeros(3 * max(maxit, 1))
+        sing = C.c_int64(-1)
+        uf, us, ur = (LEVEL[q] for q in prec)
+        f = self.lib.orc_gmres_lse
+        f.restype = C.c_int
+        rc = f(_i64(m), _i64(n), _i64(p), _p(A), _p(B), _p(b), _p(d), C.c_double(tol), _i64(maxit),
+               C.c_int(uf), C.c_int(us), C.c_int(ur), C.c_int(0 if precond == "left" else 1),
+               C.c_double(alpha_scale), _p(x), _p(r), _p(v), C.byref(st), C.byref(it),
+               C.byref(inner), _p(hist), C.byref(sing))
+        if rc:
+            raise OracleError(rc, sing.value)
+        return OracleResult(x, r, v, STATUS[st.value], it.value,
+                            hist[: 3 * it.value].reshape(-1, 3), inner=inner.value)
 
     def lse_direct(self, A, B, b, d):
         m, n = A.shape

@@ -66,6 +66,13 @@ int orc_lse_correction(int64_t m, int64_t n, int64_t p, const double* A, const d
 int orc_gls_correction(int64_t n, int64_t m, int64_t p, const double* W, const double* V,
                        const double* f1, const double* f2, const double* f3, int uf,
                        double* dy, double* dz, double* dx, int64_t* sing);
+/* GMRES-IR (inc/krylov.hpp:545 gmres_refine_lse), reference build only:
+ * precond 0 = left, 1 = bd_split; inner = total GMRES iterations */
+int orc_gmres_lse(int64_t m, int64_t n, int64_t p, const double* A, const double* B,
+                  const double* b, const double* d, double tol, int64_t maxit, int uf, int us,
+                  int ur, int precond, double alpha_scale, double* x, double* r, double* v,
+                  int32_t* status, int64_t* iters, int64_t* inner, double* hist, int64_t* sing);
+
 /* binary64 direct solves (the err-2 / er-2 denominators, inc/experiment.hpp:50-73) */
 int orc_lse_direct(int64_t m, int64_t n, int64_t p, const double* A, const double* B,
                    const double* b, const double* d, double* x, double* r, double* v,

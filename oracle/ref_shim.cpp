@@ -11,6 +11,7 @@
 //   lse_correction_solve inc/lse.hpp:84, gls_correction_solve inc/gls.hpp:107
 //   lse_direct inc/lse.hpp:132, gls_direct inc/gls.hpp:85
 //   gen_lse_problem / gen_gls_problem inc/generate.hpp:60-106
+//   gmres_refine_lse inc/krylov.hpp:545
 #include <algorithm>
 #include <atomic>
 #include <cstring>
@@ -20,6 +21,7 @@
 #include "mixedls/errors.hpp"
 #include "mixedls/generate.hpp"
 #include "mixedls/gls.hpp"
+#include "mixedls/krylov.hpp"
 #include "mixedls/lse.hpp"
 
 #include "orc_api.h"
@@ -126,6 +128,25 @@ int orc_mplse(int64_t m, int64_t n, int64_t p, const double* A, const double* B,
             put(res.state.r, r);
             put(res.state.v, v);
             put_trace(res.trace, status, iters, hist, phases);
+        },
+        sing);
+}
+
+int orc_gmres_lse(int64_t m, int64_t n, int64_t p, const double* A, const double* B,
+                  const double* b, const double* d, double tol, int64_t maxit, int uf, int us,
+                  int ur, int precond, double alpha_scale, double* x, double* r, double* v,
+                  int32_t* status, int64_t* iters, int64_t* inner, double* hist, int64_t* sing) {
+    return guarded(
+        [&] {
+            auto pb = make_lse(m, n, p, A, B, b, d);
+            auto res = gmres_refine_lse(pb, make_cfg(tol, maxit, uf, us, ur),
+                                        precond == 0 ? precond_choice::left : precond_choice::bd_split,
+                                        alpha_scale);
+            put(res.state.x, x);
+            put(res.state.r, r);
+            put(res.state.v, v);
+            put_trace(res.trace, status, iters, hist, nullptr);
+            if (inner) *inner = static_cast<int64_t>(res.trace.inner_iterations);
         },
         sing);
 }

@@ -45,6 +45,7 @@ from .api import (  # noqa: F401
     RefinementConfig,
     RefinementTrace,
     gls_direct,
+    gmres_refine_lse,
     lse_direct,
     mpgls,
     mpgls_batched,
@@ -55,6 +56,6 @@ from .api import (  # noqa: F401
 __all__ = [
     "LseProblem", "GlsProblem", "LseState", "GlsState", "PrecisionConfig", "RefinementConfig",
     "RefinementTrace", "MplseResult", "MpglsResult", "mplse", "mpgls", "mplse_batched",
-    "mpgls_batched", "lse_direct", "gls_direct", "MixedlsError", "DimensionError", "InvalidInput", "SingularTriangular",
+    "mpgls_batched", "lse_direct", "gls_direct", "gmres_refine_lse", "MixedlsError", "DimensionError", "InvalidInput", "SingularTriangular",
     "CudaError", "Unsupported", "lib", "lib_path",
 ]

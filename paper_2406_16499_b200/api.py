@@ -231,6 +231,50 @@ def mpgls(pb: GlsProblem, cfg: RefinementConfig | None = None, stream=None) -> M
     return MpglsResult(GlsState(x, y, z), _trace_from(tr, hist))
 
 
+def gmres_refine_lse(pb: LseProblem, cfg: RefinementConfig | None = None,
+                     precond: str = "bd_split", alpha_scale: float = 1.0,
+                     stream=None) -> MplseResult:
+    """GMRES-IR for LSE (gmres_refine_lse, inc/krylov.hpp:545-689) on the GPU:
+    precond "left" or "bd_split"; trace.inner_iterations = total GMRES steps."""
+    cfg = cfg or RefinementConfig()
+    ccfg = cfg.to_c()
+    if precond not in ("left", "bd_split"):
+        raise _capi.InvalidInput("gmres: precond must be 'left' or 'bd_split'")
+    dev = _is_cuda(pb.A)
+    if dev:
+        import torch
+
+        A, B, b, d = pb.A, pb.B, pb.b, pb.d
+        m, n, lda = _matrix_ld(A)
+        p, _, ldb = _matrix_ld(B)
+        x = torch.empty(n, dtype=torch.float64, device=A.device)
+        r = torch.empty(m, dtype=torch.float64, device=A.device)
+        v = torch.empty(p, dtype=torch.float64, device=A.device)
+    else:
+        A = np.asfortranarray(pb.A, dtype=np.float64)
+        B = np.asfortranarray(pb.B, dtype=np.float64)
+        if A.ndim != 2 or B.ndim != 2 or B.shape[1] != A.shape[1]:
+            raise _capi.DimensionError("lse_problem: A and B column counts differ")
+        b = np.ascontiguousarray(pb.b, dtype=np.float64)
+        d = np.ascontiguousarray(pb.d, dtype=np.float64)
+        m, n = A.shape
+        p = B.shape[0]
+        if b.shape != (m,) or d.shape != (p,):
+            raise _capi.DimensionError("lse_problem: rhs length mismatch")
+        lda, ldb = max(m, 1), max(p, 1)
+        x, r, v = np.zeros(n), np.zeros(m), np.zeros(p)
+    hist = np.zeros(3 * max(int(cfg.maxit), 1))
+    tr = Trace()
+    tr.residual_history = hist.ctypes.data_as(C.POINTER(C.c_double))
+    sing = C.c_int64(-1)
+    ex = _exec(dev, stream)
+    rc = lib.mlsb_gmres_lse(_ptr(A), lda, _ptr(B), ldb, _ptr(b), _ptr(d), m, n, p, C.byref(ccfg),
+                            0 if precond == "left" else 1, float(alpha_scale), _ptr(x), _ptr(r),
+                            _ptr(v), C.byref(tr), C.byref(sing), C.byref(ex))
+    raise_for(rc, sing.value)
+    return MplseResult(LseState(x, r, v), _trace_from(tr, hist))
+
+
 def lse_direct(pb: LseProblem, stream=None) -> LseState:
     """binary64 direct LSE solve on the GPU: the err-2 reference of the experiment
     harness (detail::lse_direct_reference, inc/experiment.hpp:50-59)."""

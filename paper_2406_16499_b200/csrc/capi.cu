@@ -138,7 +138,8 @@ int solve_large(const Shape& s, int esz, const void* A, int64_t lda, const void*
                 const void* b, const void* d, const mlsb_config* cfg, void* o1, void* o2, void* o3,
                 mlsb_trace* trace, int64_t* singular_index, const mlsb_exec* ex, bool cplx,
                 int32_t* status_out = nullptr, int64_t* iters_out = nullptr,
-                int32_t* err_out = nullptr, double* hist_out = nullptr) {
+                int32_t* err_out = nullptr, double* hist_out = nullptr, int gmres = 0,
+                double alpha_scale = 1.0) {
   const bool dev = ex && ex->pointer_kind == MLSB_DEVICE;
   cudaStream_t st = ex ? static_cast<cudaStream_t>(ex->stream) : nullptr;
   cudaError_t e;
@@ -154,6 +155,8 @@ int solve_large(const Shape& s, int esz, const void* A, int64_t lda, const void*
   P.u_s = cfg->u_s;
   P.u_r = cfg->u_r;
   P.cplx = cplx;
+  P.gmres = gmres;
+  P.alpha_scale = alpha_scale;
   if (dev) {
     P.A = A;
     P.lda = lda;
@@ -218,7 +221,7 @@ int solve_large(const Shape& s, int esz, const void* A, int64_t lda, const void*
   if (trace) {
     trace->status = out.status;
     trace->iterations = out.iters;
-    trace->inner_iterations = 0;
+    trace->inner_iterations = out.inner;
     for (int k = 0; k < 6; ++k) trace->phase_seconds[k] = out.phases[k];
     if (trace->residual_history)
       memcpy(trace->residual_history, out.hist.data(), sizeof(double) * out.hist.size());
@@ -691,6 +694,30 @@ int mlsb_gls_direct(const double* W, int64_t ldw, const double* V, int64_t ldv, 
   const mlsb_config c = direct_config();
   return solve_single(gls_shape(n, m, p), W, ldw, V, ldv, nullptr, d, &c, x, y, z, nullptr,
                       singular_index, exec);
+}
+
+int mlsb_gmres_lse(const double* A, int64_t lda, const double* B, int64_t ldb, const double* b,
+                   const double* d, int64_t m, int64_t n, int64_t p, const mlsb_config* cfg,
+                   int precond, double alpha_scale, double* x, double* r, double* v,
+                   mlsb_trace* trace, int64_t* singular_index, const mlsb_exec* exec) {
+  // gmres_refine_lse (krylov.hpp:545): same validation as mplse
+  if (m <= 0 || n <= 0 || p <= 0) return fail(MLSB_ERR_DIMENSION, "lse_problem: empty matrix");
+  if (p > n || n > m + p)
+    return fail(MLSB_ERR_DIMENSION, "lse_problem: requires p <= n <= m + p");
+  if (lda < m || ldb < p) return fail(MLSB_ERR_DIMENSION, "lse_problem: leading dimension too small");
+  if (!A || !B || !b || !d) return fail(MLSB_ERR_DIMENSION, "lse_problem: null input");
+  if (int rc = check_config(cfg)) return rc;
+  if (precond != MLSB_PRECOND_LEFT && precond != MLSB_PRECOND_BD_SPLIT)
+    return fail(MLSB_ERR_INVALID_INPUT, "gmres: unknown preconditioner");
+  if (!(alpha_scale > 0.0)) return fail(MLSB_ERR_INVALID_INPUT, "gmres: alpha_scale must be positive");
+  if (cfg->u_f != MLSB_LOW || m < n)
+    return fail(MLSB_ERR_UNSUPPORTED, "gmres: built for u_f = low and m >= n");
+  if (int rc = check_device()) return rc;
+  DevScope scope(exec);
+  if (!scope.ok) return fail(MLSB_ERR_CUDA, "cudaSetDevice failed");
+  return solve_large(lse_shape(m, n, p), 8, A, lda, B, ldb, b, d, cfg, x, r, v, trace,
+                     singular_index, exec, false, nullptr, nullptr, nullptr, nullptr,
+                     precond == MLSB_PRECOND_LEFT ? 1 : 2, alpha_scale);
 }
 
 int mlsb_mplse_z(const double* A, int64_t lda, const double* B, int64_t ldb, const double* b,

@@ -418,13 +418,293 @@ static cudaError_t rq_stage(FT* M, int64_t ld, int rb, int rr, int cb, int cc, F
   return cudaSuccess;
 }
 
+// ------------------------------------------------------------- GMRES-IR (LSE)
+// gmres_refine_lse (krylov.hpp:545-689) on the large path's factors: the
+// augmented operator is applied matrix-free to the scaled binary64 A, B (exact
+// division, like the reference's scaled copy); the preconditioners work on the
+// binary32 factors widened to binary64 (promote_factors is exact).
+struct GmBuf {
+  double* p = nullptr;
+  cudaStream_t s = nullptr;
+  ~GmBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+__global__ void k_add_div(const double* x, double s, int n, double* y) {  // y += x / s
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) y[i] += x[i] / s;
+}
+__global__ void k_finite_flag(const double* x, int n, int* flag) {
+  for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT)
+    if (!isfinite(x[i])) atomicOr(flag, 1);
+}
+
+// out = [alpha u1 + A u3; B u3; A^T u1 + B^T u2]  (augmented_operator::apply, krylov.hpp:62-77)
+static void gm_op(int m, int n, int p, double alpha, const double* gA, const double* gB,
+                  int64_t lda, int64_t ldb, double sA, double sB, const double* u, double* out,
+                  double* rpart, double* cpart, cudaStream_t st) {
+  const int R = m + p, C = n;
+  const int ntr = (R + RTR - 1) / RTR, ntc = (C + RTC - 1) / RTC;
+  const StackX SX{gA, gB, lda, ldb, m, true, sA, sB};
+  dim3 g2(ntr, ntc);
+  k_resid_tile<double, StackX><<<g2, KT, 0, st>>>(SX, R, C, u + R, u, rpart, cpart);
+  k_op_reduce<<<nblk(R + C), KT, 0, st>>>(R, C, m, ntc, ntr, rpart, cpart, u, alpha, out);
+}
+
+static void gm_dot(const double* x, const double* y, int n, double* part, int nb, double* out,
+                   cudaStream_t st) {
+  k_dot_part<<<nb, KT, 0, st>>>(x, y, n, part);
+  k_dot_final<<<1, 32, 0, st>>>(part, nb, out);
+}
+
+// block-diagonal split preconditioner, m >= n (bd_lse_apply, krylov.hpp:253-287)
+template <class FT>
+static void gm_bd(bool left, int m, int n, int p, double alpha, const FT* M, int64_t ld,
+                  const Fac<FT>& FQ, const double* w, double* out, double* ta, double* tb,
+                  double* ypart, cudaStream_t st) {
+  const double ra = 1.0 / sqrt(alpha), sa = sqrt(alpha);
+  const Mask up{1, 0, 0};
+  if (left) {
+    k_copy<double><<<nblk(p), KT, 0, st>>>(w + m, p, ta);
+    trsv<FT, double>(M, ld, m, n - p, p, false, ta, st);                 // t = R^-1 w2
+    gemv_n<FT, double>(M, ld, n - p, p, n - p, p, up, ta, out + m, st);  // o2 = T(n-p:n, n-p:n) t
+    k_copy<double><<<nblk(n), KT, 0, st>>>(w + m + p, n, tb);
+    apply_F<FT, double>(FQ, true, tb, ypart, st);                        // q = Q w3
+    trsv<FT, double>(M, ld, 0, 0, n, true, tb, st);                      // T1^T o3 = q
+    k_scal<<<nblk(m), KT, 0, st>>>(ra, w, m, out);
+    k_scal<<<nblk(p), KT, 0, st>>>(ra, out + m, p, out + m);
+    k_scal<<<nblk(n), KT, 0, st>>>(sa, tb, n, out + m + p);
+  } else {
+    gemv_h<FT, double>(M, ld, n - p, p, n - p, p, up, w + m, ta, st);    // t = T(..)^T w2
+    trsv<FT, double>(M, ld, m, n - p, p, true, ta, st);                  // R^T o2 = t
+    k_copy<double><<<nblk(n), KT, 0, st>>>(w + m + p, n, tb);
+    trsv<FT, double>(M, ld, 0, 0, n, false, tb, st);                     // T1 t3 = w3
+    apply_F<FT, double>(FQ, false, tb, ypart, st);                       // o3 = Q^T t3
+    k_scal<<<nblk(m), KT, 0, st>>>(ra, w, m, out);
+    k_scal<<<nblk(p), KT, 0, st>>>(ra, ta, p, out + m);
+    k_scal<<<nblk(n), KT, 0, st>>>(sa, tb, n, out + m + p);
+  }
+}
+
+// left preconditioner (left_lse_apply, krylov.hpp:209-230)
+template <class FT>
+static void gm_left(int m, int n, int p, double alpha, const FT* M, int64_t ld, const Fac<FT>& FZ,
+                    const Fac<FT>& FQ, const double* w, double* out, double* const* cv,
+                    double* ypart, cudaStream_t st) {
+  const double ia = 1.0 / alpha;
+  const Mask up{1, 0, 0};
+  double *ta = cv[0], *tb = cv[1], *tc = cv[2], *td = cv[3], *te = cv[4], *tf = cv[5];
+  // t = B^+ w2 = Q^T [0; R^-1 w2]
+  k_copy<double><<<nblk(p), KT, 0, st>>>(w + m, p, ta);
+  trsv<FT, double>(M, ld, m, n - p, p, false, ta, st);
+  k_fill<double><<<nblk(n), KT, 0, st>>>(tb, n, 0.0);
+  k_copy<double><<<nblk(p), KT, 0, st>>>(ta, p, tb + n - p);
+  apply_F<FT, double>(FQ, false, tb, ypart, st);
+  // h = w1 - A t, A t = Z T Q t
+  k_copy<double><<<nblk(n), KT, 0, st>>>(tb, n, tc);
+  apply_F<FT, double>(FQ, true, tc, ypart, st);
+  gemv_n<FT, double>(M, ld, 0, m, 0, n, up, tc, td, st);
+  apply_F<FT, double>(FZ, false, td, ypart, st);
+  k_sub<double><<<nblk(m), KT, 0, st>>>(w, td, m, td);
+  // g = w3 - (1/alpha) A^T h, A^T h = Q^T T^T Z^T h
+  k_copy<double><<<nblk(m), KT, 0, st>>>(td, m, te);
+  apply_F<FT, double>(FZ, true, te, ypart, st);
+  gemv_h<FT, double>(M, ld, 0, m, 0, n, up, te, tf, st);
+  apply_F<FT, double>(FQ, false, tf, ypart, st);
+  k_scal<<<nblk(n), KT, 0, st>>>(-ia, tf, n, tf);
+  k_axpy<<<nblk(n), KT, 0, st>>>(1.0, w + m + p, n, tf);
+  // o2 = (B^+)^T g = R^-T (Q g)(n-p:n)
+  apply_F<FT, double>(FQ, true, tf, ypart, st);
+  trsv<FT, double>(M, ld, m, n - p, p, true, tf + (n - p), st);
+  k_scal<<<nblk(m), KT, 0, st>>>(ia, td, m, out);
+  k_copy<double><<<nblk(p), KT, 0, st>>>(tf + (n - p), p, out + m);
+  k_copy<double><<<nblk(n), KT, 0, st>>>(tb, n, out + m + p);
+}
+
+// lse_correction_solve (lse.hpp:83-128) at binary64 on the widened factors
+template <class FT>
+static void gm_cascade(int m, int n, int p, const FT* M, int64_t ld, const Fac<FT>& FZ,
+                       const Fac<FT>& FQ, const double* f1, const double* f2, const double* f3,
+                       double* const* cv, double* ypart, double* dr, double* dv, double* dx,
+                       cudaStream_t st) {
+  const int k = n - p;
+  const Mask none{0, 0, 0};
+  double *u = cv[0], *w = cv[1], *y2 = cv[2], *q1 = cv[3], *t4 = cv[4], *y = cv[5], *tq = cv[7];
+  k_copy<double><<<nblk(n), KT, 0, st>>>(f3, n, u);
+  k_copy<double><<<nblk(m), KT, 0, st>>>(f1, m, w);
+  k_copy<double><<<nblk(p), KT, 0, st>>>(f2, p, y2);
+  apply_F<FT, double>(FQ, true, u, ypart, st);                   // u = Q f3
+  apply_F<FT, double>(FZ, true, w, ypart, st);                   // w = Z^T f1
+  trsv<FT, double>(M, ld, m, n - p, p, false, y2, st);           // R y2 = f2
+  k_copy<double><<<nblk(k), KT, 0, st>>>(u, k, q1);
+  trsv<FT, double>(M, ld, 0, 0, k, true, q1, st);                // T11^T q1 = u1
+  gemv_n<FT, double>(M, ld, 0, k, k, p, none, y2, t4, st);
+  gemv_n<FT, double>(M, ld, k, m - k, k, p, Mask{1, 0, 0}, y2, t4 + k, st);
+  k_subsub<double><<<nblk(k), KT, 0, st>>>(w, q1, t4, k, y);
+  k_copy<double><<<nblk(k), KT, 0, st>>>(q1, k, w);
+  k_sub<double><<<nblk(m - k), KT, 0, st>>>(w + k, t4 + k, m - k, w + k);
+  k_copy<double><<<nblk(m), KT, 0, st>>>(w, m, dr);
+  k_copy<double><<<nblk(p), KT, 0, st>>>(y2, p, y + k);
+  trsv<FT, double>(M, ld, 0, 0, k, false, y, st);
+  apply_F<FT, double>(FQ, false, y, ypart, st);                  // dx = Q^T y
+  apply_F<FT, double>(FZ, false, dr, ypart, st);                 // dr = Z q
+  gemv_h<FT, double>(M, ld, 0, k, k, p, none, w, t4, st);
+  gemv_h<FT, double>(M, ld, k, m - k, k, p, Mask{1, 0, 0}, w + k, tq, st);
+  k_addsub<double><<<nblk(p), KT, 0, st>>>(t4, tq, u + k, p, t4);
+  trsv<FT, double>(M, ld, m, n - p, p, true, t4, st);            // R^T dv = s
+  k_copy<double><<<nblk(n), KT, 0, st>>>(y, n, dx);
+  k_copy<double><<<nblk(p), KT, 0, st>>>(t4, p, dv);
+}
+
+// One GMRES-IR correction (krylov.hpp:640-681): rhs from the residual blocks,
+// optional cascade initial guess (left), full MGS-GMRES with Givens rotations
+// (krylov.hpp:436-512, rel_tol 1e-6, max_iter N) and the state update.
+template <class FT>
+static int gmres_correction(int kind, int m, int n, int p, double alpha, const FT* M, int64_t ld,
+                            const Fac<FT>& FZ, const Fac<FT>& FQ, const double* gA, const double* gB,
+                            int64_t lda, int64_t ldb, double sA, double sB, const double* rout,
+                            const double* cout, double* sw, double* su, double* rhs, double* wacc,
+                            double* t1, double* t2, double* t3, double* t4, double* part, int nb,
+                            double* hdev, GmBuf& bas, int& cap, double* const* cv, double* ypart,
+                            double* rpart, double* cpart, int* flag, int64_t* its_out,
+                            cudaStream_t st) {
+  const int N = m + p + n;
+  const double sqa = sqrt(alpha);
+  cudaError_t e;
+  k_scal<<<nblk(m + p), KT, 0, st>>>(sqa, rout, m + p, rhs);
+  k_scal<<<nblk(n), KT, 0, st>>>(1.0 / sqa, cout, n, rhs + m + p);
+  k_fill<double><<<nblk(N), KT, 0, st>>>(wacc, N, 0.0);
+  if (kind == 1) {  // cascade initial guess: the left preconditioner is singular on null(B)
+    gm_cascade<FT>(m, n, p, M, ld, FZ, FQ, rout, rout + m, cout, cv, ypart, t1, t1 + m, t1 + m + p, st);
+    k_scal<<<nblk(m), KT, 0, st>>>(1.0 / sqa, t1, m, wacc);
+    k_scal<<<nblk(p), KT, 0, st>>>(-1.0 / sqa, t1 + m, p, wacc + m);
+    k_scal<<<nblk(n), KT, 0, st>>>(sqa, t1 + m + p, n, wacc + m + p);
+    gm_op(m, n, p, alpha, gA, gB, lda, ldb, sA, sB, wacc, t2, rpart, cpart, st);
+    k_axpy<<<nblk(N), KT, 0, st>>>(-1.0, t2, N, rhs);
+  }
+  auto lp = [&](const double* in, double* o) {
+    if (kind == 2) gm_bd<FT>(true, m, n, p, alpha, M, ld, FQ, in, o, cv[8], cv[9], ypart, st);
+    else gm_left<FT>(m, n, p, alpha, M, ld, FZ, FQ, in, o, cv, ypart, st);
+  };
+  auto rp = [&](const double* in, double* o) {
+    gm_bd<FT>(false, m, n, p, alpha, M, ld, FQ, in, o, cv[8], cv[9], ypart, st);
+  };
+  auto grow = [&](int need) -> cudaError_t {
+    if (need <= cap) return cudaSuccess;
+    int nc = cap ? cap : 32;
+    while (nc < need) nc *= 2;
+    if (nc > N + 1) nc = N + 1;
+    double* np_ = nullptr;
+    cudaError_t ee = cudaMallocAsync(reinterpret_cast<void**>(&np_), sizeof(double) * size_t(N) * nc, st);
+    if (ee) return ee;
+    if (bas.p) {
+      cudaMemcpyAsync(np_, bas.p, sizeof(double) * size_t(N) * cap, cudaMemcpyDeviceToDevice, st);
+      cudaFreeAsync(bas.p, st);
+    }
+    bas.p = np_;
+    bas.s = st;
+    cap = nc;
+    return cudaSuccess;
+  };
+  if ((e = grow(2))) return MLSB_ERR_CUDA;
+  auto V = [&](int i) { return bas.p + size_t(i) * N; };
+  lp(rhs, V(0));
+  gm_dot(V(0), V(0), N, part, nb, hdev, st);
+  double hb[2];
+  cudaMemcpyAsync(hb, hdev, 8, cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;
+  const double beta = sqrt(hb[0]);
+  int64_t its = 0;
+  if (beta != 0.0) {
+    k_scal<<<nblk(N), KT, 0, st>>>(1.0 / beta, V(0), N, V(0));
+    std::vector<std::vector<double>> H;
+    std::vector<double> gc, gs, g{beta}, hh;
+    int k = 0;
+    for (; k < N; ++k) {
+      if ((e = grow(k + 2))) return MLSB_ERR_CUDA;
+      if (kind == 2) {
+        rp(V(k), t3);
+        gm_op(m, n, p, alpha, gA, gB, lda, ldb, sA, sB, t3, t4, rpart, cpart, st);
+      } else {
+        gm_op(m, n, p, alpha, gA, gB, lda, ldb, sA, sB, V(k), t4, rpart, cpart, st);
+      }
+      lp(t4, t2);
+      for (int i = 0; i <= k; ++i) {  // modified Gram-Schmidt
+        gm_dot(t2, V(i), N, part, nb, hdev + i, st);
+        k_axpy_dev<<<nblk(N), KT, 0, st>>>(hdev + i, V(i), N, t2);
+      }
+      gm_dot(t2, t2, N, part, nb, hdev + k + 1, st);
+      hh.assign(k + 2, 0.0);
+      cudaMemcpyAsync(hh.data(), hdev, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, st);
+      if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;
+      std::vector<double> h(hh);
+      const double hk1 = sqrt(hh[k + 1]);
+      h[k + 1] = hk1;
+      const bool breakdown = hk1 <= 0x1p-52 * beta;
+      for (int i = 0; i < k; ++i) {
+        const double t = gc[i] * h[i] + gs[i] * h[i + 1];
+        h[i + 1] = -gs[i] * h[i] + gc[i] * h[i + 1];
+        h[i] = t;
+      }
+      const double r = std::hypot(h[k], h[k + 1]);
+      const double c = r == 0.0 ? 1.0 : h[k] / r;
+      const double s = r == 0.0 ? 0.0 : h[k + 1] / r;
+      gc.push_back(c);
+      gs.push_back(s);
+      h[k] = r;
+      h[k + 1] = 0.0;
+      g.push_back(-s * g[k]);
+      g[k] = c * g[k];
+      H.push_back(std::move(h));
+      its = k + 1;
+      if (std::abs(g[k + 1]) <= 1e-6 * beta) {
+        ++k;
+        break;
+      }
+      if (breakdown) {
+        ++k;
+        break;
+      }
+      k_scal<<<nblk(N), KT, 0, st>>>(1.0 / hk1, t2, N, V(k + 1));
+    }
+    // back-substitute H y = g over the k columns, x = sum y_i V_i
+    std::vector<double> y(k, 0.0);
+    for (int jj = k; jj-- > 0;) {
+      double sacc = g[jj];
+      for (int i = jj + 1; i < k; ++i) sacc -= H[i][jj] * y[i];
+      y[jj] = sacc / H[jj][jj];
+    }
+    k_fill<double><<<nblk(N), KT, 0, st>>>(t3, N, 0.0);
+    for (int i = 0; i < k; ++i) k_axpy<<<nblk(N), KT, 0, st>>>(y[i], V(i), N, t3);
+    if (kind == 2) {
+      rp(t3, t4);
+      k_axpy<<<nblk(N), KT, 0, st>>>(1.0, t4, N, wacc);
+    } else {
+      k_axpy<<<nblk(N), KT, 0, st>>>(1.0, t3, N, wacc);
+    }
+  }
+  *its_out = its;
+  // r += sqa w1, v -= sqa w2, x += w3 / sqa (krylov.hpp:677-679), then the finite check
+  k_axpy<<<nblk(m), KT, 0, st>>>(sqa, wacc, m, sw);
+  k_axpy<<<nblk(p), KT, 0, st>>>(-sqa, wacc + m, p, sw + m);
+  k_add_div<<<nblk(n), KT, 0, st>>>(wacc + m + p, sqa, n, su);
+  k_finite_flag<<<nblk(m + p), KT, 0, st>>>(sw, m + p, flag);
+  k_finite_flag<<<nblk(n), KT, 0, st>>>(su, n, flag);
+  if ((e = cudaGetLastError())) return MLSB_ERR_CUDA;
+  return MLSB_OK;
+}
+
 // --------------------------------------------------------------- driver
 template <class FT, class WT, class CT>
 static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   const bool lse = P.kind == KIND_LSE;
   constexpr bool kReal = std::is_same<WT, double>::value;
+  constexpr bool kGm = kReal && std::is_same<CT, double>::value;  // GMRES-IR instantiation
   const bool ext = kReal && P.u_r == 2;
   const int m = int(P.m), n = int(P.n), p = int(P.p);
+  // GMRES-IR is built for real LSE with m >= n (the first case of the split
+  // preconditioner, krylov.hpp:259-269; the reference's configs C1, C3)
+  if (P.gmres && (!kGm || !lse || m < n)) return MLSB_ERR_UNSUPPORTED;
   const int R = lse ? m + p : n, C = lse ? n : m + p;
   const int64_t ld = R;
   const int kq = lse ? p : std::min(n, p);  // RQ reflectors
@@ -508,7 +788,20 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
     memcpy(&v, &b, 8);
     return v == 0.0 ? 1.0 : v;
   };
-  const double sA = asd(hb[0]), sB = asd(hb[1]), c1 = asd(hb[2]);
+  const double sA = asd(hb[0]), c1 = asd(hb[2]);
+  double sB = asd(hb[1]);
+  if (P.gmres) {
+    // gmres_refine_lse (krylov.hpp:562-566): s_B = s_A ||B||_F / ||A||_F balances the blocks
+    k_cast<FT, WT><<<grid, KT, 0, st>>>(gA, P.lda, rows1, cols1, 1.0, M, ld, parts);
+    k_sum_parts<<<1, 32, 0, st>>>(parts, grid, nsum + 0);
+    k_cast<FT, WT><<<grid, KT, 0, st>>>(gB, P.ldb, rows2, cols2, 1.0, M + m, ld, parts + grid);
+    k_sum_parts<<<1, 32, 0, st>>>(parts + grid, grid, nsum + 1);
+    double hr[2];
+    cudaMemcpyAsync(hr, nsum, sizeof(hr), cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;
+    const double nAr = hr[0] > 0 ? sqrt(hr[0]) : 1.0, nBr = hr[1] > 0 ? sqrt(hr[1]) : 1.0;
+    sB = sA * nBr / nAr;
+  }
   const double c2 = lse ? sB * c1 / sA : c1;  // LSE c_d = s_B c_b / s_A ; GLS c_d
   // right-hand sides (exact division, lse.hpp:326-329)
   if (lse) {
@@ -684,6 +977,42 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   int status = 1;
   int64_t pass = 0;
   out->hist.clear();
+  // ------------------------------------------------ GMRES-IR state (LSE)
+  // Vectors of the augmented system, N = m + p + n, ordered [r-block; v-block;
+  // x-block]; the Krylov basis grows on demand (full, unrestarted MGS-GMRES,
+  // krylov.hpp:436-512, max_iter = N).
+  const int N = m + p + n;
+  GmBuf gbuf, gbas;
+  double *g_rhs = nullptr, *g_w = nullptr, *g_t1 = nullptr, *g_t2 = nullptr, *g_t3 = nullptr,
+         *g_t4 = nullptr, *g_part = nullptr, *g_h = nullptr;
+  int g_cap = 0;
+  double g_alpha = 1.0;
+  const int g_nb = 148 * 2;
+  if constexpr (kGm) {
+    if (P.gmres) {
+      gbuf.s = gbas.s = st;
+      const size_t nv = size_t(N);
+      if ((e = cudaMallocAsync(reinterpret_cast<void**>(&gbuf.p),
+                               sizeof(double) * (6 * nv + g_nb + 2 * (size_t(N) + 2)), st)))
+        return MLSB_ERR_CUDA;
+      g_rhs = gbuf.p;
+      g_w = g_rhs + nv;
+      g_t1 = g_w + nv;
+      g_t2 = g_t1 + nv;
+      g_t3 = g_t2 + nv;
+      g_t4 = g_t3 + nv;
+      g_part = g_t4 + nv;
+      g_h = g_part + g_nb;
+      // alpha = alpha_scale * ||r0|| (krylov.hpp:613)
+      k_dot_part<<<g_nb, KT, 0, st>>>(sw, sw, m, g_part);
+      k_dot_final<<<1, 32, 0, st>>>(g_part, g_nb, g_h);
+      double r2 = 0.0;
+      cudaMemcpyAsync(&r2, g_h, 8, cudaMemcpyDeviceToHost, st);
+      if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;
+      g_alpha = P.alpha_scale * (r2 > 0.0 ? sqrt(r2) : 1.0);
+    }
+  }
+  out->inner = 0;
   for (pass = 1; pass <= P.maxit; ++pass) {
     // row initialisers and weights of this pass
     if (lse) {
@@ -783,6 +1112,18 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       break;
     }
 
+    if constexpr (kGm) {
+      if (P.gmres) {
+        int64_t its = 0;
+        int rc = gmres_correction(P.gmres, m, n, p, g_alpha, M, ld, FZ, FQ, gA, gB, P.lda, P.ldb, sA,
+                                  sB, rout, cout, sw, su, g_rhs, g_w, g_t1, g_t2, g_t3, g_t4, g_part,
+                                  g_nb, g_h, gbas, g_cap, cv, ypart, rpart, cpart, flags + 3, &its,
+                                  st);
+        if (rc) return rc;
+        out->inner += its;
+        continue;
+      }
+    }
     // ---- correction at u_s (demotion by one sigma, refine.hpp:103-107)
     const unsigned long long* sb = lows ? bits + 5 : nullptr;
     if (lse) {  // Algorithm 1 (lse.hpp:83-128)
@@ -876,7 +1217,7 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   out->phases[5] = (ms[0] + ms[4]) * 1e-3;  // other
   out->phases[0] = ms[1] * 1e-3;            // factorization
   out->phases[1] = ms[2] * 1e-3;            // init
-  out->phases[2] = ms[3] * 1e-3;            // residual + correction (loop)
+  out->phases[P.gmres ? 4 : 2] = ms[3] * 1e-3;  // the refinement loop (residual + correction | gmres)
   out->phases[3] = 0.0;
   out->phases[4] = 0.0;
   for (auto& x : ev) cudaEventDestroy(x);
@@ -894,7 +1235,7 @@ int large_solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
     if (P.u_s != 0) return solve<cf, cd, cd>(P, st, out);
     return solve<cf, cd, cf>(P, st, out);
   }
-  if (P.u_s != 0) return solve<float, double, double>(P, st, out);
+  if (P.u_s != 0 || P.gmres) return solve<float, double, double>(P, st, out);  // GMRES: binary64 factors
   return solve<float, double, float>(P, st, out);
 }
 

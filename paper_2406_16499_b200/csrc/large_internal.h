@@ -55,12 +55,17 @@ struct LargeProblem {
   int64_t maxit;
   int u_f, u_s, u_r;
   bool cplx;
+  // GMRES-IR (krylov.hpp:545-689): 0 = classical IR, 1 = left preconditioner,
+  // 2 = block-diagonal split preconditioner; alpha = alpha_scale * ||r0||
+  int gmres = 0;
+  double alpha_scale = 1.0;
 };
 struct LargeOut {
   int status = 1;
   int64_t iters = 0;
   int err = 0;
   int64_t sing = -1;
+  int64_t inner = 0;  // GMRES iterations summed over the passes
   std::vector<double> hist;
   double phases[6] = {0, 0, 0, 0, 0, 0};
 };

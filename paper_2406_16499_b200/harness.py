@@ -11,9 +11,10 @@ host side, around the GPU solvers.
   format (``std::to_chars`` without a format: shortest digits, the shorter of
   fixed / scientific, fixed on a tie).
 
-Methods: ``"direct"`` and ``"ir"`` (classical IR, mplse / mpgls).  The
-reference's ``"gmres-left"`` / ``"gmres-bd"`` (inc/krylov.hpp) are not built
-on the GPU yet: they report status ``"unsupported"``.
+Methods: ``"direct"``, ``"ir"`` (classical IR, mplse / mpgls) and, for LSE,
+``"gmres-left"`` / ``"gmres-bd"`` (GMRES-IR, gmres_refine_lse,
+inc/krylov.hpp:545-689).  GMRES-IR for GLS is not built on the GPU yet: it
+reports status ``"unsupported"``.
 """
 from __future__ import annotations
 
@@ -241,6 +242,14 @@ def run_experiment(problem, spec: GeneratorSpec, method: str,
             st = res.state
             rep.status = res.trace.status
             rep.iterations = res.trace.iterations
+            rep.timing.update({k: float(res.trace.timing.get(k, 0.0)) for k in rep.timing})
+        elif lse:
+            res = api.gmres_refine_lse(problem, cfg,
+                                       precond="left" if method == "gmres-left" else "bd_split")
+            st = res.state
+            rep.status = res.trace.status
+            rep.iterations = res.trace.iterations
+            rep.inner_iterations = res.trace.inner_iterations
             rep.timing.update({k: float(res.trace.timing.get(k, 0.0)) for k in rep.timing})
         else:
             rep.status = "unsupported"

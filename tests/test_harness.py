@@ -137,8 +137,13 @@ def test_run_experiment_c1(gpu):
     assert rd.status == "converged" and rd.metric1 < 1e-14 and rd.metric2 == 0.0
     assert ri.status == "converged" and 1 <= ri.iterations <= 10
     assert ri.metric1 < 1e-13 and ri.metric2 < 1e-10
-    assert rg.status == "unsupported"
+    assert rg.status == "converged" and rg.inner_iterations >= 1 and rg.metric2 < 1e-10
+    rgl = H.run_experiment(pb, spec, "gmres-left", cfg)
+    assert rgl.status == "converged" and rgl.inner_iterations >= 1
     W, V, dg = G.gls_problem(200, 100, 150, 1e4, 1e2, 2)
     rgls = H.run_experiment(gpu.GlsProblem(W, V, dg), H.GeneratorSpec("gls", 100, 200, 150, 1e4, 2),
                             "ir", gpu.RefinementConfig(maxit=10))
     assert rgls.status == "converged" and rgls.metric1 < 1e-13 and rgls.metric2 < 1e-10
+    rgg = H.run_experiment(gpu.GlsProblem(W, V, dg), H.GeneratorSpec("gls", 100, 200, 150, 1e4, 2),
+                           "gmres-bd", gpu.RefinementConfig(maxit=10))
+    assert rgg.status == "unsupported"

@@ -296,89 +296,144 @@ static cudaError_t gemm(bool ha, bool hb, int Mr, int N, int K, double alpha, co
 }
 
 // ----------------------------------------------- blocked GRQ / GQR at u_f
-// Look-ahead: after panel b, the columns (rows, for RQ) of panel b+1 are
-// updated first; panel b+1 is then factored by its cluster on the
-// high-priority stream `s2` while the remaining trailing update of panel b
-// (the big GEMM) runs on `st` over the other SMs.
+// Two-level blocking.  Panels of NB = 32 reflectors are factored by one
+// cluster each (panel_factor); NBO / NB consecutive panels form an outer
+// block whose own columns (rows, for RQ) are brought up to date by rank-NB
+// updates, and whose merged compact-WY form (V: L x NBO, T: NBO x NBO,
+// k_tmerge) then updates the whole trailing matrix in ONE rank-NBO product --
+// three GEMMs with K = NBO or K = L instead of K = NB, the arithmetic
+// intensity the FP32 FFMA roofline needs.
+//
+// Look-ahead: after outer block B, the columns (rows) of block B+1 are
+// updated first; block B+1 is then factored (panels, inner updates, T merge)
+// on the high-priority stream `s2` while the remaining trailing update of
+// block B (the big GEMMs) runs on `st` over the other SMs.
+struct WsBuf {
+  void* W;
+  void* W2;
+  void* work;
+  size_t wn;
+};
 struct Streams {
   cudaStream_t st, s2;
   cudaEvent_t ev_upd, ev_pan;
+  WsBuf ws[2];   // [0] for st, [1] for s2 (inner updates and Gram products)
+  void* G;       // NBO x NBO Gram matrix of the block factored on s2
+  void* TB[2];   // merged T of alternating outer blocks, NBO x NBO
 };
 
 // C2 := P^H C2 = C2 - V T^H (V^H C2) for C2 = M[j0:j0+L, c0:c0+nc]
 template <class FT>
 static cudaError_t qr_update(FT* M, int64_t ld, int j0, int L, int nbk, int c0, int nc, const FT* V,
-                             const FT* Tb, FT* W, FT* W2, FT* work, size_t wn, cudaStream_t st) {
+                             int64_t ldv, const FT* Tb, int ldt, const WsBuf& w, cudaStream_t st) {
   if (nc <= 0) return cudaSuccess;
   cudaError_t e;
+  FT* W = static_cast<FT*>(w.W);
+  FT* W2 = static_cast<FT*>(w.W2);
+  FT* work = static_cast<FT*>(w.work);
   FT* C2 = M + j0 + int64_t(c0) * ld;
-  if ((e = gemm<FT>(true, false, nbk, nc, L, 1.0, V, L, C2, ld, 0.0, W, NB, work, wn, st))) return e;
-  if ((e = gemm<FT>(true, false, nbk, nc, nbk, 1.0, Tb, NB, W, NB, 0.0, W2, NB, nullptr, 0, st))) return e;
-  return gemm<FT>(false, false, L, nc, nbk, -1.0, V, L, W2, NB, 1.0, C2, ld, nullptr, 0, st);
-}
-
-// QR of M[0:rows, 0:k] (columns), trailing columns up to cend
-template <class FT>
-static cudaError_t qr_stage(FT* M, int64_t ld, int rows, int k, int cend, FT* Vbuf, FT* Tbuf,
-                            FT* taus, FT* W, FT* W2, FT* work, size_t wn, Fac<FT>& F,
-                            const Streams& S) {
-  cudaError_t e;
-  const int np = (k + NB - 1) / NB;
-  std::vector<size_t> voff(np + 1, 0);
-  for (int b = 0; b < np; ++b) voff[b + 1] = voff[b] + size_t(rows - b * NB) * NB;
-  auto V_of = [&](int b) { return Vbuf + voff[b]; };
-  auto T_of = [&](int b) { return Tbuf + size_t(b) * NB * NB; };
-  if (np == 0) return cudaSuccess;
-  if ((e = panel_factor<FT>(M, ld, 0, 0, rows, std::min(NB, k), false, taus, V_of(0), rows, T_of(0), 0,
-                            S.st)))
-    return e;
-  for (int b = 0; b < np; ++b) {
-    const int j0 = b * NB, nbk = std::min(NB, k - j0), L = rows - j0;
-    if (b > 0) cudaStreamWaitEvent(S.st, S.ev_pan, 0);  // panel b was factored on s2
-    F.b.push_back(Blk<FT>{V_of(b), L, L, nbk, T_of(b), j0});
-    const int c1 = j0 + nbk;
-    if (b + 1 < np) {
-      const int nbn = std::min(NB, k - c1);
-      if ((e = qr_update<FT>(M, ld, j0, L, nbk, c1, nbn, V_of(b), T_of(b), W, W2, work, wn, S.st))) return e;
-      cudaEventRecord(S.ev_upd, S.st);
-      cudaStreamWaitEvent(S.s2, S.ev_upd, 0);
-      if ((e = panel_factor<FT>(M, ld, c1, c1, rows - c1, nbn, false, taus + c1, V_of(b + 1), rows - c1,
-                                T_of(b + 1), 0, S.s2)))
-        return e;
-      cudaEventRecord(S.ev_pan, S.s2);
-      if ((e = qr_update<FT>(M, ld, j0, L, nbk, c1 + nbn, cend - c1 - nbn, V_of(b), T_of(b), W, W2, work,
-                             wn, S.st)))
-        return e;
-    } else {
-      if ((e = qr_update<FT>(M, ld, j0, L, nbk, c1, cend - c1, V_of(b), T_of(b), W, W2, work, wn, S.st)))
-        return e;
-    }
-  }
-  return cudaSuccess;
+  if ((e = gemm<FT>(true, false, nbk, nc, L, 1.0, V, ldv, C2, ld, 0.0, W, nbk, work, w.wn, st))) return e;
+  if ((e = gemm<FT>(true, false, nbk, nc, nbk, 1.0, Tb, ldt, W, nbk, 0.0, W2, nbk, nullptr, 0, st))) return e;
+  return gemm<FT>(false, false, L, nc, nbk, -1.0, V, ldv, W2, nbk, 1.0, C2, ld, nullptr, 0, st);
 }
 
 // rows [r0, r0+nr) of M[:, cb : cb+L] := (...) P = (...) - ((...) V) T V^H
 template <class FT>
 static cudaError_t rq_update(FT* M, int64_t ld, int r0, int nr, int cb, int L, int nbk, const FT* V,
-                             const FT* Tb, FT* W, FT* W2, FT* work, size_t wn, cudaStream_t st) {
+                             int64_t ldv, const FT* Tb, int ldt, const WsBuf& w, cudaStream_t st) {
   if (nr <= 0) return cudaSuccess;
   cudaError_t e;
+  FT* W = static_cast<FT*>(w.W);
+  FT* W2 = static_cast<FT*>(w.W2);
+  FT* work = static_cast<FT*>(w.work);
   FT* Ma = M + r0 + int64_t(cb) * ld;
-  if ((e = gemm<FT>(false, false, nr, nbk, L, 1.0, Ma, ld, V, L, 0.0, W, nr, work, wn, st))) return e;
-  if ((e = gemm<FT>(false, false, nr, nbk, nbk, 1.0, W, nr, Tb, NB, 0.0, W2, nr, nullptr, 0, st))) return e;
-  return gemm<FT>(false, true, nr, L, nbk, -1.0, W2, nr, V, L, 1.0, Ma, ld, nullptr, 0, st);
+  if ((e = gemm<FT>(false, false, nr, nbk, L, 1.0, Ma, ld, V, ldv, 0.0, W, nr, work, w.wn, st))) return e;
+  if ((e = gemm<FT>(false, false, nr, nbk, nbk, 1.0, W, nr, Tb, ldt, 0.0, W2, nr, nullptr, 0, st))) return e;
+  return gemm<FT>(false, true, nr, L, nbk, -1.0, W2, nr, V, ldv, 1.0, Ma, ld, nullptr, 0, st);
+}
+
+// merged T of an outer block (nbo reflectors, V: L x nbo at ld L) into Tout
+template <class FT>
+static cudaError_t block_t(int L, int nbo, const FT* V, const FT* Tp, FT* Tout, const Streams& S,
+                          cudaStream_t st) {
+  FT* G = static_cast<FT*>(S.G);
+  const WsBuf& w = S.ws[1];
+  cudaError_t e;
+  if ((e = gemm<FT>(true, false, nbo, nbo, L, 1.0, V, L, V, L, 0.0, G, nbo, static_cast<FT*>(w.work), w.wn,
+                    st)))
+    return e;
+  if constexpr (tr<FT>::cplx) return tmerge_c64(nbo, G, nbo, Tp, Tout, NBO, st);
+  else return tmerge_f32(nbo, G, nbo, Tp, Tout, NBO, st);
+}
+
+// QR of M[0:rows, 0:k] (columns), trailing columns up to cend.
+// V of outer block B: (rows - B NBO) x NBO dense at ld rows - B NBO (zeros
+// above each panel's unit diagonal); panel j's T at Tbuf + j NB NB.
+template <class FT>
+static cudaError_t qr_stage(FT* M, int64_t ld, int rows, int k, int cend, FT* Vbuf, FT* Tbuf,
+                            FT* taus, Fac<FT>& F, const Streams& S) {
+  cudaError_t e;
+  const int nob = (k + NBO - 1) / NBO;
+  if (nob == 0) return cudaSuccess;
+  std::vector<size_t> voff(nob + 1, 0);
+  for (int B = 0; B < nob; ++B) voff[B + 1] = voff[B] + size_t(rows - B * NBO) * NBO;
+  if ((e = cudaMemsetAsync(Vbuf, 0, voff[nob] * sizeof(FT), S.st))) return e;
+  auto TBof = [&](int B) { return static_cast<FT*>(S.TB[B & 1]); };
+  // panels, inner updates and the T merge of block B, on stream s
+  auto factor_block = [&](int B, cudaStream_t s, const WsBuf& w) -> cudaError_t {
+    const int j0 = B * NBO, nbo = std::min(NBO, k - j0), L0 = rows - j0;
+    FT* Vb = Vbuf + voff[B];
+    cudaError_t e2;
+    for (int c = j0; c < j0 + nbo; c += NB) {
+      const int nbk = std::min(NB, j0 + nbo - c), o = c - j0;
+      FT* Vp = Vb + o + int64_t(o) * L0;
+      FT* Tp = Tbuf + size_t(c / NB) * NB * NB;
+      if ((e2 = panel_factor<FT>(M, ld, c, c, rows - c, nbk, false, taus + c, Vp, L0, Tp, 0, s))) return e2;
+      if ((e2 = qr_update<FT>(M, ld, c, rows - c, nbk, c + nbk, j0 + nbo - c - nbk, Vp, L0, Tp, NB, w, s)))
+        return e2;
+    }
+    if (nbo > NB) return block_t<FT>(L0, nbo, Vb, Tbuf + size_t(j0 / NB) * NB * NB, TBof(B), S, s);
+    return cudaSuccess;
+  };
+  if ((e = factor_block(0, S.st, S.ws[0]))) return e;
+  for (int B = 0; B < nob; ++B) {
+    const int j0 = B * NBO, nbo = std::min(NBO, k - j0), L0 = rows - j0;
+    const FT* Vb = Vbuf + voff[B];
+    const FT* Tb = nbo > NB ? TBof(B) : Tbuf + size_t(j0 / NB) * NB * NB;
+    const int ldt = nbo > NB ? NBO : NB;
+    if (B > 0) cudaStreamWaitEvent(S.st, S.ev_pan, 0);  // block B was factored on s2
+    for (int c = j0; c < j0 + nbo; c += NB)
+      F.b.push_back(Blk<FT>{Vb + (c - j0) + int64_t(c - j0) * L0, L0, rows - c, std::min(NB, j0 + nbo - c),
+                            Tbuf + size_t(c / NB) * NB * NB, c});
+    const int c1 = j0 + nbo;
+    if (B + 1 < nob) {
+      const int nbn = std::min(NBO, k - c1);
+      if ((e = qr_update<FT>(M, ld, j0, L0, nbo, c1, nbn, Vb, L0, Tb, ldt, S.ws[0], S.st))) return e;
+      cudaEventRecord(S.ev_upd, S.st);
+      cudaStreamWaitEvent(S.s2, S.ev_upd, 0);
+      if ((e = factor_block(B + 1, S.s2, S.ws[1]))) return e;
+      cudaEventRecord(S.ev_pan, S.s2);
+      if ((e = qr_update<FT>(M, ld, j0, L0, nbo, c1 + nbn, cend - c1 - nbn, Vb, L0, Tb, ldt, S.ws[0], S.st)))
+        return e;
+    } else {
+      if ((e = qr_update<FT>(M, ld, j0, L0, nbo, c1, cend - c1, Vb, L0, Tb, ldt, S.ws[0], S.st))) return e;
+    }
+  }
+  return cudaSuccess;
 }
 
 // RQ of the block rows [rb, rb+rr) x columns [cb, cb+cc) (rows bottom-up), applied
-// from the right to every row above; panels of NB rows from the bottom.
+// from the right to every row above; panels of NB rows from the bottom, NBO / NB
+// panels per outer block.
 template <class FT>
 static cudaError_t rq_stage(FT* M, int64_t ld, int rb, int rr, int cb, int cc, FT* Vbuf, FT* Tbuf,
-                            FT* taus, FT* W, FT* W2, FT* work, size_t wn, Fac<FT>& F,
-                            const Streams& S) {
+                            FT* taus, Fac<FT>& F, const Streams& S) {
   cudaError_t e;
   const int kk = std::min(rr, cc);
   const int np = (kk + NB - 1) / NB;
   if (np == 0) return cudaSuccess;
+  constexpr int PPB = NBO / NB;  // panels per outer block
+  const int nob = (np + PPB - 1) / PPB;
   // panel b: reflectors j in [r1 - nbk, r1), r1 = kk - b NB; row of j = rb + rr - kk + j,
   // pivot column = cb + cc - kk + j
   auto r1_of = [&](int b) { return kk - b * NB; };
@@ -386,33 +441,51 @@ static cudaError_t rq_stage(FT* M, int64_t ld, int rb, int rr, int cb, int cc, F
   auto row_first = [&](int b) { return int64_t(rb + rr - kk + r1_of(b) - 1); };
   auto pcmax = [&](int b) { return int64_t(cb + cc - kk + r1_of(b) - 1); };
   auto L_of = [&](int b) { return int(pcmax(b) - cb + 1); };
-  std::vector<size_t> voff(np + 1, 0);
-  for (int b = 0; b < np; ++b) voff[b + 1] = voff[b] + size_t(L_of(b)) * NB;
-  auto V_of = [&](int b) { return Vbuf + voff[b]; };
-  auto T_of = [&](int b) { return Tbuf + size_t(b) * NB * NB; };
-  auto factor = [&](int b, cudaStream_t s) {
-    return panel_factor<FT>(M, ld, row_first(b), pcmax(b), L_of(b), nbk_of(b), true,
-                            taus + size_t(b) * NB, V_of(b), L_of(b), T_of(b), cb, s);
+  auto above_of = [&](int b) { return int(row_first(b) - (nbk_of(b) - 1)); };  // rows [0, above)
+  auto pend = [&](int B) { return std::min(np, (B + 1) * PPB); };
+  auto nbo_of = [&](int B) { return r1_of(B * PPB) - (pend(B) < np ? r1_of(pend(B)) : 0); };
+  std::vector<size_t> voff(nob + 1, 0);
+  for (int B = 0; B < nob; ++B) voff[B + 1] = voff[B] + size_t(L_of(B * PPB)) * NBO;
+  if ((e = cudaMemsetAsync(Vbuf, 0, voff[nob] * sizeof(FT), S.st))) return e;
+  auto TBof = [&](int B) { return static_cast<FT*>(S.TB[B & 1]); };
+  auto Vp_of = [&](int b) { return Vbuf + voff[b / PPB] + size_t(b % PPB) * NB * L_of((b / PPB) * PPB); };
+  auto factor_block = [&](int B, cudaStream_t s, const WsBuf& w) -> cudaError_t {
+    const int L0 = L_of(B * PPB), bend = pend(B);
+    cudaError_t e2;
+    for (int b = B * PPB; b < bend; ++b) {
+      FT* Tp = Tbuf + size_t(b) * NB * NB;
+      if ((e2 = panel_factor<FT>(M, ld, row_first(b), pcmax(b), L_of(b), nbk_of(b), true,
+                                 taus + size_t(b) * NB, Vp_of(b), L0, Tp, cb, s)))
+        return e2;
+      const int nrem = above_of(b) - above_of(bend - 1);  // rows of the block's later panels
+      if ((e2 = rq_update<FT>(M, ld, above_of(b) - nrem, nrem, cb, L_of(b), nbk_of(b), Vp_of(b), L0, Tp, NB,
+                              w, s)))
+        return e2;
+    }
+    const int nbo = nbo_of(B);
+    if (nbo > NB) return block_t<FT>(L0, nbo, Vbuf + voff[B], Tbuf + size_t(B * PPB) * NB * NB, TBof(B), S, s);
+    return cudaSuccess;
   };
-  if ((e = factor(0, S.st))) return e;
-  for (int b = 0; b < np; ++b) {
-    if (b > 0) cudaStreamWaitEvent(S.st, S.ev_pan, 0);
-    const int L = L_of(b), nbk = nbk_of(b);
-    F.b.push_back(Blk<FT>{V_of(b), L, L, nbk, T_of(b), 0});
-    const int above = int(row_first(b) - (nbk - 1));  // rows [0, above)
-    if (b + 1 < np) {
-      const int nbn = nbk_of(b + 1);
-      if ((e = rq_update<FT>(M, ld, above - nbn, nbn, cb, L, nbk, V_of(b), T_of(b), W, W2, work, wn, S.st)))
-        return e;
+  if ((e = factor_block(0, S.st, S.ws[0]))) return e;
+  for (int B = 0; B < nob; ++B) {
+    if (B > 0) cudaStreamWaitEvent(S.st, S.ev_pan, 0);
+    const int L0 = L_of(B * PPB), nbo = nbo_of(B), bend = pend(B);
+    const FT* Vb = Vbuf + voff[B];
+    const FT* Tb = nbo > NB ? TBof(B) : Tbuf + size_t(B * PPB) * NB * NB;
+    const int ldt = nbo > NB ? NBO : NB;
+    for (int b = B * PPB; b < bend; ++b)
+      F.b.push_back(Blk<FT>{Vp_of(b), L0, L_of(b), nbk_of(b), Tbuf + size_t(b) * NB * NB, 0});
+    const int above = above_of(bend - 1);
+    if (B + 1 < nob) {
+      const int nbn = nbo_of(B + 1);
+      if ((e = rq_update<FT>(M, ld, above - nbn, nbn, cb, L0, nbo, Vb, L0, Tb, ldt, S.ws[0], S.st))) return e;
       cudaEventRecord(S.ev_upd, S.st);
       cudaStreamWaitEvent(S.s2, S.ev_upd, 0);
-      if ((e = factor(b + 1, S.s2))) return e;
+      if ((e = factor_block(B + 1, S.s2, S.ws[1]))) return e;
       cudaEventRecord(S.ev_pan, S.s2);
-      if ((e = rq_update<FT>(M, ld, 0, above - nbn, cb, L, nbk, V_of(b), T_of(b), W, W2, work, wn, S.st)))
-        return e;
+      if ((e = rq_update<FT>(M, ld, 0, above - nbn, cb, L0, nbo, Vb, L0, Tb, ldt, S.ws[0], S.st))) return e;
     } else {
-      if ((e = rq_update<FT>(M, ld, 0, above, cb, L, nbk, V_of(b), T_of(b), W, W2, work, wn, S.st)))
-        return e;
+      if ((e = rq_update<FT>(M, ld, 0, above, cb, L0, nbo, Vb, L0, Tb, ldt, S.ws[0], S.st))) return e;
     }
   }
   return cudaSuccess;
@@ -710,30 +783,39 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   const int kq = lse ? p : std::min(n, p);  // RQ reflectors
   const int kz = lse ? std::min(m, n) : m;  // QR reflectors
   const int nbz = (kz + NB - 1) / NB, nbq = (kq + NB - 1) / NB;
+  const int obz = (kz + NBO - 1) / NBO, obq = (kq + NBO - 1) / NBO;  // outer blocks
   const int ntr = (R + RTR - 1) / RTR, ntc = (C + RTC - 1) / RTC;
   const int L = std::max(R, C);
-  const size_t wn = size_t(NB) * std::max(R, C) * 64;  // split-K partials
+  const size_t wn = size_t(NB) * std::max(R, C) * 64;  // split-K partials (st)
+  const size_t wn2 = size_t(NBO) * NBO * 64;            // split-K partials (s2)
   const bool lows = sizeof(CT) == sizeof(FT);
 
   Arena ar;
-  const size_t bytes = sizeof(FT) * (size_t(R) * C + size_t(nbz) * R * NB + size_t(nbq) * C * NB +
-                                     size_t(nbz + nbq) * NB * NB + size_t(C + R) + 2 * size_t(R) * NB +
-                                     wn + 8 * size_t(L)) +
+  const size_t bytes = sizeof(FT) * (size_t(R) * C + size_t(obz) * R * NBO + size_t(obq) * C * NBO +
+                                     size_t(nbz + nbq) * NB * NB + size_t(C + R) + 2 * size_t(L) * NBO +
+                                     wn + 8 * size_t(L) + 2 * size_t(NB) * NBO + wn2 +
+                                     3 * size_t(NBO) * NBO) +
                        sizeof(WT) * (size_t(R) * (6 + ntc) + size_t(C) * (5 + ntr)) +
                        (ext ? 16 * (size_t(ntc) * R + size_t(ntr) * C) + 8 * size_t(R) : 0) +
                        sizeof(CT) * (10 * size_t(L) + 32 * 256) + 64 * 1024 + 64 * 256;
   cudaError_t e = ar.init(bytes + bytes / 4 + (1 << 20), st);
   if (e) return MLSB_ERR_CUDA;
   FT* M = ar.take<FT>(size_t(R) * C);
-  FT* VZ = ar.take<FT>(size_t(nbz) * R * NB);
-  FT* VQ = ar.take<FT>(size_t(nbq) * C * NB);
+  FT* VZ = ar.take<FT>(size_t(obz) * R * NBO);
+  FT* VQ = ar.take<FT>(size_t(obq) * C * NBO);
   FT* TZ = ar.take<FT>(size_t(nbz) * NB * NB);
   FT* TQ = ar.take<FT>(size_t(nbq) * NB * NB);
   FT* tauZ = ar.take<FT>(C);
   FT* tauQ = ar.take<FT>(size_t(nbq) * NB + R);
-  FT* W = ar.take<FT>(size_t(L) * NB);
-  FT* W2 = ar.take<FT>(size_t(L) * NB);
+  FT* W = ar.take<FT>(size_t(L) * NBO);
+  FT* W2 = ar.take<FT>(size_t(L) * NBO);
   FT* gw = ar.take<FT>(wn);
+  FT* Ws2 = ar.take<FT>(size_t(NB) * NBO);
+  FT* W2s2 = ar.take<FT>(size_t(NB) * NBO);
+  FT* gw2 = ar.take<FT>(wn2);
+  FT* Gs2 = ar.take<FT>(size_t(NBO) * NBO);
+  FT* TB0 = ar.take<FT>(size_t(NBO) * NBO);
+  FT* TB1 = ar.take<FT>(size_t(NBO) * NBO);
   FT* fv[8];
   for (int i = 0; i < 8; ++i) fv[i] = ar.take<FT>(L);
   WT* rinit = ar.take<WT>(R);
@@ -852,6 +934,11 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   // ---------------------------------------------------------- GRQ / GQR
   Streams SS;
   SS.st = st;
+  SS.ws[0] = WsBuf{W, W2, gw, wn};
+  SS.ws[1] = WsBuf{Ws2, W2s2, gw2, wn2};
+  SS.G = Gs2;
+  SS.TB[0] = TB0;
+  SS.TB[1] = TB1;
   {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -869,11 +956,11 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   } sguard{SS};
   Fac<FT> FZ, FQ;  // QR factor (Z for LSE, Q for GLS) / RQ factor (Q^H for LSE, Z^H for GLS)
   if (lse) {
-    if ((e = rq_stage<FT>(M, ld, m, p, 0, n, VQ, TQ, tauQ, W, W2, gw, wn, FQ, SS))) return MLSB_ERR_CUDA;
-    if ((e = qr_stage<FT>(M, ld, m, kz, n, VZ, TZ, tauZ, W, W2, gw, wn, FZ, SS))) return MLSB_ERR_CUDA;
+    if ((e = rq_stage<FT>(M, ld, m, p, 0, n, VQ, TQ, tauQ, FQ, SS))) return MLSB_ERR_CUDA;
+    if ((e = qr_stage<FT>(M, ld, m, kz, n, VZ, TZ, tauZ, FZ, SS))) return MLSB_ERR_CUDA;
   } else {
-    if ((e = qr_stage<FT>(M, ld, n, kz, m + p, VZ, TZ, tauZ, W, W2, gw, wn, FZ, SS))) return MLSB_ERR_CUDA;
-    if ((e = rq_stage<FT>(M, ld, 0, n, m, p, VQ, TQ, tauQ, W, W2, gw, wn, FQ, SS))) return MLSB_ERR_CUDA;
+    if ((e = qr_stage<FT>(M, ld, n, kz, m + p, VZ, TZ, tauZ, FZ, SS))) return MLSB_ERR_CUDA;
+    if ((e = rq_stage<FT>(M, ld, 0, n, m, p, VQ, TQ, tauQ, FQ, SS))) return MLSB_ERR_CUDA;
   }
   // zero pivots in the order of the reference's first failing trsv
   // (LSE: R at lse.hpp:53, then T11 at :60; GLS: T22 at gls.hpp:55, then R at :61)

@@ -15,9 +15,12 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 #include "large_common.cuh"
 #include "large_internal.h"
+#include "../../include/mixedls_b200_tools.h"
 
 namespace mlsb {
 namespace lg {
@@ -139,6 +142,199 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, T alpha,
   }
 }
 
+// binary32 128x128 tile for the rank-NBO trailing updates (K = 128 or K = L):
+// BK = 16, 256 threads, 8x8 outputs per thread as 2x2 sub-blocks of 4x4
+// (rows tr*4 + {0..3} and 64 + tr*4 + {0..3}; columns likewise), so every
+// fragment read is one LDS.128 (4 per kk for 64 FFMA) and a warp's epilogue
+// covers 64 consecutive rows of two columns.  Global tiles are read as float4
+// along the operand's contiguous dimension when pointer and leading dimension
+// allow it (VEC), staged in registers while the previous tile is consumed,
+// and transposed into the k-major shared layout on the store.
+template <bool HA, bool HB, bool VEC>
+__global__ void __launch_bounds__(256, 2) sgemm128(int M, int N, int K, float alpha,
+                                                   const float* __restrict__ A, int64_t lda,
+                                                   const float* __restrict__ B, int64_t ldb, float beta,
+                                                   float* __restrict__ C, int64_t ldc, int kchunk,
+                                                   int64_t split_stride) {
+  constexpr int BM = 128, BN = 128, BK = 16, LDS = BM + 4;
+  __shared__ __align__(16) float As[2][BK][LDS];
+  __shared__ __align__(16) float Bs[2][BK][LDS];
+  const int tid = threadIdx.x, tr = tid & 15, tc = tid >> 4;
+  const int i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
+  const int kbeg = blockIdx.z * kchunk;
+  const int kend = min(K, kbeg + kchunk);
+  C += int64_t(blockIdx.z) * split_stride;
+
+  // staging: 512 float4 slots per operand tile, two per thread
+  float ra[8], rb[8];
+  // op(A)(i,k): !HA -> A[i + k lda] (contiguous in i) ; HA -> A[k + i lda] (contiguous in k)
+  auto load_a = [&](int k0) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int slot = tid + 256 * s;
+      if (!HA) {  // 4 consecutive rows i of one k
+        const int i = (slot & 31) * 4, k = slot >> 5;
+        const int gi = i0 + i, gk = k0 + k;
+        if (VEC) {
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (gk < kend && gi < M) v = *reinterpret_cast<const float4*>(A + gi + int64_t(gk) * lda);
+          ra[4 * s] = v.x, ra[4 * s + 1] = v.y, ra[4 * s + 2] = v.z, ra[4 * s + 3] = v.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            ra[4 * s + t] = (gk < kend && gi + t < M) ? A[gi + t + int64_t(gk) * lda] : 0.f;
+        }
+      } else {  // 4 consecutive k of one row i
+        const int k = (slot & 3) * 4, i = slot >> 2;
+        const int gi = i0 + i, gk = k0 + k;
+        if (VEC) {
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (gi < M && gk < kend) v = *reinterpret_cast<const float4*>(A + gk + int64_t(gi) * lda);
+          ra[4 * s] = v.x, ra[4 * s + 1] = v.y, ra[4 * s + 2] = v.z, ra[4 * s + 3] = v.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            ra[4 * s + t] = (gi < M && gk + t < kend) ? A[gk + t + int64_t(gi) * lda] : 0.f;
+        }
+      }
+    }
+  };
+  // op(B)(k,j): !HB -> B[k + j ldb] (contiguous in k) ; HB -> B[j + k ldb] (contiguous in j)
+  auto load_b = [&](int k0) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int slot = tid + 256 * s;
+      if (HB) {
+        const int j = (slot & 31) * 4, k = slot >> 5;
+        const int gj = j0 + j, gk = k0 + k;
+        if (VEC) {
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (gk < kend && gj < N) v = *reinterpret_cast<const float4*>(B + gj + int64_t(gk) * ldb);
+          rb[4 * s] = v.x, rb[4 * s + 1] = v.y, rb[4 * s + 2] = v.z, rb[4 * s + 3] = v.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            rb[4 * s + t] = (gk < kend && gj + t < N) ? B[gj + t + int64_t(gk) * ldb] : 0.f;
+        }
+      } else {
+        const int k = (slot & 3) * 4, j = slot >> 2;
+        const int gj = j0 + j, gk = k0 + k;
+        if (VEC) {
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (gj < N && gk < kend) v = *reinterpret_cast<const float4*>(B + gk + int64_t(gj) * ldb);
+          rb[4 * s] = v.x, rb[4 * s + 1] = v.y, rb[4 * s + 2] = v.z, rb[4 * s + 3] = v.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            rb[4 * s + t] = (gj < N && gk + t < kend) ? B[gk + t + int64_t(gj) * ldb] : 0.f;
+        }
+      }
+    }
+  };
+  float acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+  auto store_a = [&](int buf) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int slot = tid + 256 * s;
+      if (!HA) {
+        const int i = (slot & 31) * 4, k = slot >> 5;
+        *reinterpret_cast<float4*>(&As[buf][k][i]) = make_float4(ra[4 * s], ra[4 * s + 1], ra[4 * s + 2], ra[4 * s + 3]);
+      } else {
+        const int k = (slot & 3) * 4, i = slot >> 2;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) As[buf][k + t][i] = ra[4 * s + t];
+      }
+    }
+  };
+  auto store_b = [&](int buf) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int slot = tid + 256 * s;
+      if (HB) {
+        const int j = (slot & 31) * 4, k = slot >> 5;
+        *reinterpret_cast<float4*>(&Bs[buf][k][j]) = make_float4(rb[4 * s], rb[4 * s + 1], rb[4 * s + 2], rb[4 * s + 3]);
+      } else {
+        const int k = (slot & 3) * 4, j = slot >> 2;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) Bs[buf][k + t][j] = rb[4 * s + t];
+      }
+    }
+  };
+  // one kk step: 4 LDS.128, 64 FFMA
+  auto step = [&](int buf, int kk) {
+    const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][tr * 4]);
+    const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + tr * 4]);
+    const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tc * 4]);
+    const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tc * 4]);
+    const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float bf[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(af[a], bf[b], acc[a][b]);
+  };
+
+
+  int buf = 0;
+  if (kbeg < kend) {
+    load_a(kbeg);
+    store_a(0);
+    load_b(kbeg);
+    store_b(0);
+  }
+  __syncthreads();
+  // the next tile is staged half at a time (A during kk 0..7, B during kk
+  // 8..15) so only 8 staging registers are live
+  for (int k0 = kbeg; k0 < kend; k0 += BK) {
+    const bool more = k0 + BK < kend;
+    if (more) load_a(k0 + BK);
+#pragma unroll
+    for (int kk = 0; kk < BK / 2; ++kk) step(buf, kk);
+    if (more) {
+      store_a(buf ^ 1);
+      load_b(k0 + BK);
+    }
+#pragma unroll
+    for (int kk = BK / 2; kk < BK; ++kk) step(buf, kk);
+    if (more) store_b(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  // epilogue: column by column, 4-row groups (float4 when aligned)
+  const bool cvec = VEC && ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && (ldc & 3) == 0 && (i0 & 3) == 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const int gj = j0 + (b < 4 ? tc * 4 + b : 64 + tc * 4 + b - 4);
+    if (gj >= N) continue;
+    float* cj = C + int64_t(gj) * ldc;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gi = i0 + h * 64 + tr * 4;
+      if (cvec && gi + 3 < M) {
+        float4 v = make_float4(alpha * acc[4 * h][b], alpha * acc[4 * h + 1][b], alpha * acc[4 * h + 2][b],
+                               alpha * acc[4 * h + 3][b]);
+        if (beta != 0.f) {
+          const float4 o = *reinterpret_cast<const float4*>(cj + gi);
+          v.x = fmaf(beta, o.x, v.x), v.y = fmaf(beta, o.y, v.y), v.z = fmaf(beta, o.z, v.z), v.w = fmaf(beta, o.w, v.w);
+        }
+        *reinterpret_cast<float4*>(cj + gi) = v;
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (gi + t >= M) continue;
+          float v = alpha * acc[4 * h + t][b];
+          if (beta != 0.f) v = fmaf(beta, cj[gi + t], v);
+          cj[gi + t] = v;
+        }
+      }
+    }
+  }
+}
+
 // C[i + j ldc] = sum_z part[z][i + j M] + beta * C   (fixed split order)
 template <class T>
 __global__ void splitk_reduce(int M, int N, int splits, const T* __restrict__ part, int64_t stride,
@@ -211,11 +407,62 @@ static cudaError_t gemm_tile(bool ha, bool hb, int M, int N, int K, T alpha, con
   return cudaGetLastError();
 }
 
+template <bool VEC>
+static void launch128(bool ha, bool hb, dim3 grid, int M, int N, int K, float alpha, const float* A,
+                      int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc,
+                      int kchunk, int64_t sstr, cudaStream_t st) {
+  if (!ha && !hb)
+    sgemm128<false, false, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+  else if (ha && !hb)
+    sgemm128<true, false, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+  else if (!ha && hb)
+    sgemm128<false, true, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+  else
+    sgemm128<true, true, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+}
+
+static cudaError_t sgemm_sq(bool ha, bool hb, int M, int N, int K, float alpha, const float* A, int64_t lda,
+                            const float* B, int64_t ldb, float beta, float* C, int64_t ldc, float* work,
+                            size_t work_elems, cudaStream_t st) {
+  const int gm = (M + 127) / 128, gn = (N + 127) / 128;
+  int splits = 1;
+  if (K > 0 && work && alpha == 1.f && beta == 0.f) {
+    const int tiles = gm * gn;
+    while (tiles * splits < 2 * 148 && splits < 64 && K / (splits * 2) >= 128 &&
+           size_t(M) * N * (splits * 2) <= work_elems)
+      splits *= 2;
+  }
+  int kchunk = K > 0 ? (K + splits - 1) / splits : 1;
+  kchunk = (kchunk + 15) / 16 * 16;
+  // float4 operand tiles: aligned pointers, leading dimensions and contiguous
+  // extents all multiples of 4 (so no vector straddles an edge)
+  const bool vec = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (lda & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(B) & 15) == 0 && (ldb & 3) == 0 &&
+                   ((ha ? K : M) & 3) == 0 && ((hb ? N : K) & 3) == 0;
+  dim3 grid(gm, gn, splits);
+  float* Cd = splits == 1 ? C : work;
+  const int64_t ldd = splits == 1 ? ldc : M, sstr = splits == 1 ? 0 : int64_t(M) * N;
+  const float bd = splits == 1 ? beta : 0.f;
+  if (vec) launch128<true>(ha, hb, grid, M, N, K, alpha, A, lda, B, ldb, bd, Cd, ldd, kchunk, sstr, st);
+  else launch128<false>(ha, hb, grid, M, N, K, alpha, A, lda, B, ldb, bd, Cd, ldd, kchunk, sstr, st);
+  cudaError_t e = cudaGetLastError();
+  if (e || splits == 1) return e;
+  const int64_t total = int64_t(M) * N;
+  const int blocks = int(std::min<int64_t>((total + 255) / 256, 148 * 8));
+  splitk_reduce<float><<<blocks, 256, 0, st>>>(M, N, splits, work, total, 0.f, C, ldc);
+  return cudaGetLastError();
+}
+
 template <class T>
 cudaError_t gemm_t(bool ha, bool hb, int M, int N, int K, T alpha, const T* A, int64_t lda,
                    const T* B, int64_t ldb, T beta, T* C, int64_t ldc, T* work, size_t work_elems,
                    cudaStream_t st) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  if constexpr (std::is_same<T, float>::value) {
+    static const bool old_tiles = getenv("MLSB_GEMM_OLD") != nullptr;  // A/B comparisons
+    if (M > 64 && N > 64 && !old_tiles)
+      return sgemm_sq(ha, hb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, work, work_elems, st);
+  }
   if (N <= 32 && M > 32)
     return gemm_tile<T, typename Tiles<T>::Tall>(ha, hb, M, N, K, alpha, A, lda, B, ldb, beta, C,
                                                  ldc, work, work_elems, st);
@@ -224,6 +471,72 @@ cudaError_t gemm_t(bool ha, bool hb, int M, int N, int K, T alpha, const T* A, i
                                                  ldc, work, work_elems, st);
   return gemm_tile<T, typename Tiles<T>::Sq>(ha, hb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
                                              work, work_elems, st);
+}
+
+// T of an outer WY block from its NB-wide panels: P_0 P_1 ... = I - V T V^H
+// with V = [V_0 V_1 ...], so the off-diagonal block column j is
+//     T[0:jNB, j] = -T[0:jNB, 0:jNB] * (V_{0:j}^H V_j) * T_jj
+// (the block form of xLARFT's forward recursion).  G = V^H V comes from a
+// GEMM; one CTA merges the panels' T_jj (stored NB x NB, consecutive) in
+// shared memory.
+template <class T>
+__global__ void __launch_bounds__(256) k_tmerge(int nbo, const T* __restrict__ G, int ldg,
+                                                const T* __restrict__ Tp, T* __restrict__ Tout,
+                                                int ldt) {
+  extern __shared__ __align__(16) unsigned char sm_[];
+  constexpr int LDS = NBO + 1;
+  T* S = reinterpret_cast<T*>(sm_);  // S[r + c LDS], upper triangular
+  T* X = S + NBO * LDS;              // X[r + c NBO]
+  const int tid = threadIdx.x;
+  const int nblk = (nbo + NB - 1) / NB;
+  for (int e = tid; e < nbo * nbo; e += 256) {
+    const int r = e % nbo, c = e / nbo, br = r / NB, bc = c / NB;
+    S[r + c * LDS] = br == bc ? Tp[br * NB * NB + (r - br * NB) + (c - bc * NB) * NB] : zero<T>();
+  }
+  __syncthreads();
+  for (int j = 1; j < nblk; ++j) {
+    const int c0 = j * NB, w = min(NB, nbo - c0), h = c0;
+    for (int e = tid; e < h * w; e += 256) {
+      const int r = e % h, c = e / h;
+      T acc = zero<T>();
+      for (int t = 0; t <= c; ++t) mac(acc, G[r + int64_t(c0 + t) * ldg], S[(c0 + t) + (c0 + c) * LDS]);
+      X[r + c * NBO] = acc;
+    }
+    __syncthreads();
+    for (int e = tid; e < h * w; e += 256) {
+      const int r = e % h, c = e / h;
+      T acc = zero<T>();
+      for (int t = r; t < h; ++t) mac(acc, S[r + t * LDS], X[t + c * NBO]);
+      S[r + (c0 + c) * LDS] = -acc;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nbo * nbo; e += 256) {
+    const int r = e % nbo, c = e / nbo;
+    Tout[r + int64_t(c) * ldt] = S[r + c * LDS];
+  }
+}
+
+template <class T>
+static cudaError_t tmerge_t(int nbo, const T* G, int ldg, const T* Tp, T* Tout, int ldt,
+                            cudaStream_t st) {
+  if (nbo <= 0 || nbo > NBO) return cudaErrorInvalidValue;
+  const size_t sm = sizeof(T) * (size_t(NBO) * (NBO + 1) + size_t(NBO) * NB);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_tmerge<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    if (e) return e;
+    attr = true;
+  }
+  k_tmerge<T><<<1, 256, sm, st>>>(nbo, G, ldg, Tp, Tout, ldt);
+  return cudaGetLastError();
+}
+cudaError_t tmerge_f32(int nbo, const float* G, int ldg, const float* Tp, float* Tout, int ldt,
+                       cudaStream_t st) {
+  return tmerge_t<float>(nbo, G, ldg, Tp, Tout, ldt, st);
+}
+cudaError_t tmerge_c64(int nbo, const cf* G, int ldg, const cf* Tp, cf* Tout, int ldt, cudaStream_t st) {
+  return tmerge_t<cf>(nbo, G, ldg, Tp, Tout, ldt, st);
 }
 
 cudaError_t gemm_f32(bool ha, bool hb, int M, int N, int K, float alpha, const float* A,
@@ -239,3 +552,10 @@ cudaError_t gemm_c64(bool ha, bool hb, int M, int N, int K, cf alpha, const cf* 
 
 }  // namespace lg
 }  // namespace mlsb
+
+extern "C" int mlsb_wy_gemm_f32(int ta, int tb, int M, int N, int K, float alpha, const float* A,
+                                int64_t lda, const float* B, int64_t ldb, float beta, float* C,
+                                int64_t ldc, float* work, size_t work_elems, void* stream) {
+  return int(mlsb::lg::gemm_f32(ta != 0, tb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, work,
+                                work_elems, static_cast<cudaStream_t>(stream)));
+}

@@ -20,7 +20,14 @@ cudaError_t gemm_c64(bool ha, bool hb, int M, int N, int K, cf alpha, const cf* 
                      size_t work_elems, cudaStream_t st);
 
 constexpr int NB = 32;       // reflectors per panel / WY block
+constexpr int NBO = 128;     // reflectors per outer block (one trailing update)
 constexpr int PCL = 16;      // CTAs per panel cluster
+
+// Tout (nbo x nbo, ld ldt) = T of the outer block whose NB-wide panels have
+// T_j at Tp + j NB NB (ld NB) and Gram matrix G = V^H V (ld ldg).
+cudaError_t tmerge_f32(int nbo, const float* G, int ldg, const float* Tp, float* Tout, int ldt,
+                       cudaStream_t st);
+cudaError_t tmerge_c64(int nbo, const cf* G, int ldg, const cf* Tp, cf* Tout, int ldt, cudaStream_t st);
 
 // One panel of NB Householder reflectors, factored by a PCL-CTA cluster.
 // QR view P (L x nb): P[r][q] = M[r0 + r, c0 + q]           (rq = false)
@@ -34,7 +41,8 @@ constexpr int PCL = 16;      // CTAs per panel cluster
 // vbase: (RQ) M column stored in V row 0.
 template <class T>
 cudaError_t panel_factor(T* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb, bool rq, T* tau,
-                         T* V, int64_t ldv, T* Tm, int64_t vbase, cudaStream_t st);
+                         T* V, int64_t ldv, T* Tm, int64_t vbase, cudaStream_t st,
+                         long long* probe = nullptr);
 
 // One problem on the whole GPU (device pointers, column-major; WT = binary64 or
 // complex128 interleaved).  LSE: A m x n, B p x n, b, d -> x, r, v.

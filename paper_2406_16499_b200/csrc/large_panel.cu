@@ -21,8 +21,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
 #include "large_common.cuh"
 #include "large_internal.h"
+#include "../../include/mixedls_b200_tools.h"
 
 namespace cg = cooperative_groups;
 
@@ -43,6 +48,7 @@ struct PanelArgs {
   int64_t ldv;
   T* Tm;
   int64_t vbase;  // RQ: M column of V row 0
+  long long* probe = nullptr;  // clock64 stamps of CTA 0 thread 0 (measurement builds only)
 };
 
 template <class T>
@@ -233,6 +239,287 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs<T> a) {
   cl.sync();  // no CTA may exit while others still read its shared memory
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident binary32 panel (the large path's critical chain: one
+// panel per NB reflectors, 160 panels at C3).  Every thread of the cluster
+// owns RPT whole rows of the panel in registers (P[i][0..NB)), so a
+// reflector step touches shared memory only for its reductions:
+//
+//   1. per thread: d_k = sum_{own rows r > q} x_r P[r][k] for all k (and
+//      ||x||^2 in binary64) -- RPT*NB register FMAs;
+//   2. warp: transposed butterfly (31 shuffles) leaves lane k with the warp's
+//      d_k; CTA: 16 warp partials summed in warp order by thread k;
+//   3. cluster: each CTA PUSHES its partials (d, pivot row, norm) into slot
+//      [rank] of every CTA's exchange buffer (remote st.shared::cluster, no
+//      remote-load round trip), one barrier.cluster, then sums the slots in
+//      rank order -- identical totals in every CTA;
+//   4. per thread: xLARFG scalars, coef_k = tau (p_k + inv d_k), and the
+//      rank-1 update of its own rows, all in registers.
+//
+// Two CTA barriers and one cluster barrier per reflector; the q loop is fully
+// unrolled so every register index is static.
+__device__ __forceinline__ uint32_t cl_addr(const void* p, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(r)
+               : "r"(uint32_t(__cvta_generic_to_shared(p))), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cl(uint32_t a, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_cl(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+// remote store that signals the destination CTA's mbarrier on arrival
+__device__ __forceinline__ void st_async(uint32_t a, float v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(a), "f"(v),
+               "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t a, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(a), "d"(v),
+               "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(const void* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(uint32_t(__cvta_generic_to_shared(bar))),
+      "r"(parity)
+      : "memory");
+}
+// all threads of the cluster; orders the remote shared stores before the wait
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int RPT, int NT>
+__global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelArgs<float> a) {
+  constexpr int NW = NT / 32;
+  __shared__ float wpart[NW][NB];
+  __shared__ double wnorm[NW];
+  __shared__ float prow_s[NB];
+  __shared__ float xd[2][PCL][2 * NB];  // [parity][rank][d | pivot row]
+  __shared__ double xn[2][PCL];
+  __shared__ __align__(8) unsigned long long xbar[2];  // exchange arrivals, per parity
+  __shared__ uint32_t rbase[PCL];                      // cluster address of xd in CTA c
+  __shared__ __align__(16) float coef_s[NB];
+  __shared__ float scal[2];
+  __shared__ float G[NB * NB];
+  __shared__ float taus[NB];
+
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = int(cl.block_rank()), ncl = a.ncl;
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int nb = a.nb;
+  const int rb = rank * a.rc, re = min(a.L, rb + a.rc);
+
+  float P[RPT][NB];
+  int row[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    row[i] = rb + tid + NT * i;
+    const bool own = row[i] < re;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) P[i][k] = (own && k < nb) ? ld_view(a, row[i], k) : 0.f;
+    if (!own) row[i] = -1;  // never > q, never == q
+  }
+  for (int e = tid; e < NB * NB; e += NT) G[e] = 0.f;
+  const uint32_t xd0 = uint32_t(__cvta_generic_to_shared(&xd[0][0][0]));
+  if (tid < PCL) rbase[tid] = tid < ncl ? cl_addr(&xd[0][0][0], tid) : 0u;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(uint32_t(__cvta_generic_to_shared(&xbar[0]))));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(uint32_t(__cvta_generic_to_shared(&xbar[1]))));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster_barrier();  // every exchange barrier initialised before any remote signal
+  const uint32_t xbytes = uint32_t(ncl) * (2 * NB * sizeof(float) + sizeof(double));
+  // my slot in the exchange buffers and the barrier, as offsets from xd (same in every CTA)
+  const uint32_t off_slot = (tid < 2 * NB ? uint32_t(__cvta_generic_to_shared(&xd[0][rank][tid]))
+                                          : uint32_t(__cvta_generic_to_shared(&xn[0][rank]))) - xd0;
+  const uint32_t off_bar = uint32_t(__cvta_generic_to_shared(&xbar[0])) - xd0;
+  constexpr uint32_t par_d = sizeof(xd[0]), par_n = sizeof(xn[0]);
+
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    if (q < nb) {  // uniform over the cluster
+      const int par = q & 1;
+      long long* pq = (a.probe && rank == 0 && tid == 0) ? a.probe + 8 * q : nullptr;
+      if (pq) pq[0] = clock64();
+      // ---- 1. thread partials
+      float d[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) d[k] = 0.f;
+      double nn = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        if (row[i] > q) {
+          const float x = P[i][q];
+          nn = fma(double(x), double(x), nn);
+#pragma unroll
+          for (int k = 0; k < NB; ++k) d[k] = fmaf(x, P[i][k], d[k]);
+        } else if (row[i] == q) {
+#pragma unroll
+          for (int k = 0; k < NB; ++k) prow_s[k] = P[i][k];
+        }
+      }
+      // ---- 2. warp transposed reduction: lane l ends with the warp sum of d[l]
+#pragma unroll
+      for (int s = 16; s >= 1; s >>= 1) {
+        const bool up = (l & s) != 0;
+#pragma unroll
+        for (int j = 0; j < s; ++j) {
+          const float send = up ? d[j] : d[j + s];
+          const float keep = up ? d[j + s] : d[j];
+          d[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+      }
+      nn = wsum(nn);
+      wpart[w][l] = d[0];
+      if (l == 0) wnorm[w] = nn;
+      if (pq) pq[1] = clock64();
+      __syncthreads();
+      if (pq) pq[2] = clock64();
+      // ---- 3. CTA partials pushed into slot [rank] of every CTA's exchange
+      //         buffer by st.async, each landing store counted on the
+      //         destination's mbarrier (no fence, no cluster barrier)
+      if (tid == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         uint32_t(__cvta_generic_to_shared(&xbar[par]))),
+                     "r"(xbytes)
+                     : "memory");
+      if (tid <= 2 * NB) {
+        const uint32_t so = off_slot + (tid < 2 * NB ? par * par_d : par * par_n), bo = off_bar + 8 * par;
+        if (tid < 2 * NB) {
+          float v;
+          if (tid < NB) {
+            float t[NW];
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) t[ww] = wpart[ww][tid];
+            v = 0.f;
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) v += t[ww];
+          } else {
+            v = (q >= rb && q < re) ? prow_s[tid - NB] : 0.f;
+          }
+#pragma unroll
+          for (int c = 0; c < PCL; ++c)
+            if (c < ncl) st_async(rbase[c] + so, v, rbase[c] + bo);
+        } else {
+          double t[NW];
+#pragma unroll
+          for (int ww = 0; ww < NW; ++ww) t[ww] = wnorm[ww];
+          double v = 0.0;
+#pragma unroll
+          for (int ww = 0; ww < NW; ++ww) v += t[ww];
+#pragma unroll
+          for (int c = 0; c < PCL; ++c)
+            if (c < ncl) st_async(rbase[c] + so, v, rbase[c] + bo);
+        }
+      }
+      // ---- 4. warp 0: totals in rank order (lane k: d_k, p_k), xLARFG, the
+      //         update coefficients coef_k = tau v^T P[:, k] and Gram entries
+      if (pq) pq[3] = clock64();
+      if (w == 0) {
+        mbar_wait(&xbar[par], (q >> 1) & 1);
+        if (pq) pq[4] = clock64();
+        float td[PCL], tp[PCL];
+        double tn[PCL];
+#pragma unroll
+        for (int c = 0; c < PCL; ++c) {
+          const bool in = c < ncl;
+          td[c] = in ? xd[par][c][l] : 0.f;
+          tp[c] = in ? xd[par][c][NB + l] : 0.f;
+          tn[c] = in ? xn[par][c] : 0.0;
+        }
+        float dk = 0.f, pk = 0.f;
+        double nrm = 0.0;
+#pragma unroll
+        for (int c = 0; c < PCL; ++c) {
+          dk += td[c];
+          pk += tp[c];
+          nrm += tn[c];
+        }
+        float tau, inv, beta;
+        larfg_s(__shfl_sync(0xffffffffu, pk, q), nrm, tau, inv, beta);
+        coef_s[l] = l > q ? tau * fmaf(inv, dk, pk) : 0.f;
+        if (l < q) G[l + NB * q] = fmaf(inv, dk, pk);  // v_l^T v_q
+        if (l == 0) {
+          scal[0] = inv;
+          scal[1] = beta;
+          taus[q] = tau;
+        }
+      }
+      if (pq) pq[5] = clock64();
+      __syncthreads();
+      if (pq) pq[6] = clock64();
+      // ---- 5. rank-1 update of my rows, in registers
+      const float inv = scal[0], beta = scal[1];
+      float v[RPT];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) v[i] = row[i] == q ? 1.f : (row[i] > q ? inv * P[i][q] : 0.f);
+#pragma unroll
+      for (int k4 = 0; k4 < NB; k4 += 4) {
+        if (k4 + 3 > q) {
+          const float4 c4 = *reinterpret_cast<const float4*>(&coef_s[k4]);
+          const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (k4 + t > q)
+#pragma unroll
+              for (int i = 0; i < RPT; ++i) P[i][k4 + t] = fmaf(-cc[t], v[i], P[i][k4 + t]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+        if (row[i] >= q) P[i][q] = row[i] == q ? beta : v[i];
+      if (pq) pq[7] = clock64();
+    }
+  }
+  __syncthreads();
+  // ---- write back the factored panel and the dense reflector block
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int r = row[i];
+    if (r < 0) continue;
+    const int64_t vi = a.rq ? (a.c0 - r - a.vbase) : r;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      if (k >= nb) break;
+      st_view(a, r, k, P[i][k]);
+      a.V[vi + k * a.ldv] = r < k ? 0.f : (r == k ? 1.f : P[i][k]);
+    }
+  }
+  if (rank == 0) {
+    if (tid < nb) a.tau[tid] = taus[tid];
+    if (w == 0) {
+      // T[q][q] = tau_q ; T[0:q, q] = -tau_q T[0:q, 0:q] G[0:q, q]; lane l owns row l
+      float Tr[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) Tr[k] = 0.f;
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        if (q < nb) {
+          float t = 0.f;
+#pragma unroll
+          for (int k = 0; k < NB; ++k)
+            if (k < q) t = fmaf(Tr[k], G[k + NB * q], t);
+          const float tq = taus[q];
+          Tr[q] = l < q ? -(tq * t) : (l == q ? tq : 0.f);
+        }
+      }
+      if (l < nb)
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+          if (q < nb) a.Tm[l + q * NB] = Tr[q];
+    }
+  }
+  cluster_barrier();
+}
+
 template <class T>
 static size_t panel_smem(int rc) {
   const int NV = 2 * NB;
@@ -242,7 +529,7 @@ static size_t panel_smem(int rc) {
 
 template <class T>
 cudaError_t panel_factor(T* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb, bool rq, T* tau,
-                         T* V, int64_t ldv, T* Tm, int64_t vbase, cudaStream_t st) {
+                         T* V, int64_t ldv, T* Tm, int64_t vbase, cudaStream_t st, long long* probe) {
   if (nb <= 0 || nb > NB || L < nb) return cudaErrorInvalidValue;
   PanelArgs<T> a;
   a.M = M;
@@ -261,9 +548,45 @@ cudaError_t panel_factor(T* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb
   a.ldv = ldv;
   a.Tm = Tm;
   a.vbase = vbase;
+  a.probe = probe;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(PNT);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  static const bool smem_panel = getenv("MLSB_PANEL_SMEM") != nullptr;  // A/B comparisons
+  if constexpr (std::is_same<T, float>::value) {
+    // register-resident rows: 128 threads x 4 rows per CTA (one warp per SM
+    // sub-partition) while 16 CTAs hold the panel, else 512 x 2
+    if (L <= PCL * 512 * 2 && !smem_panel) {
+      const bool small = L <= PCL * 128 * 4;
+      const int per = small ? 128 * 4 : 512 * 2;
+      const int ncl = std::min(PCL, (L + per - 1) / per);
+      a.ncl = ncl;
+      a.rc = (L + ncl - 1) / ncl;
+      auto kern = small ? panel_reg_kernel<4, 128> : panel_reg_kernel<2, 512>;
+      static bool attr_reg = false;
+      if (!attr_reg) {
+        if ((e = cudaFuncSetAttribute(panel_reg_kernel<4, 128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)))
+          return e;
+        if ((e = cudaFuncSetAttribute(panel_reg_kernel<2, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)))
+          return e;
+        attr_reg = true;
+      }
+      cfg.gridDim = dim3(ncl);
+      cfg.blockDim = dim3(small ? 128 : 512);
+      cfg.dynamicSmemBytes = 0;
+      attr[0].val.clusterDim.x = ncl;
+      return cudaLaunchKernelEx(&cfg, kern, a);
+    }
+  }
   const size_t sm = panel_smem<T>(a.rc);
   auto kern = panel_kernel<T>;
-  cudaError_t e;
   static bool attr_done[2] = {false, false};
   if (!attr_done[sizeof(T) == 8]) {
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1))) return e;
@@ -272,25 +595,27 @@ cudaError_t panel_factor(T* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb
     attr_done[sizeof(T) == 8] = true;
   }
   if (sm > 227 * 1024) return cudaErrorInvalidValue;
-  cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.ncl);
-  cfg.blockDim = dim3(PNT);
   cfg.dynamicSmemBytes = sm;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = a.ncl;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template cudaError_t panel_factor<float>(float*, int64_t, int64_t, int64_t, int, int, bool, float*,
-                                         float*, int64_t, float*, int64_t, cudaStream_t);
+                                         float*, int64_t, float*, int64_t, cudaStream_t, long long*);
 template cudaError_t panel_factor<cf>(cf*, int64_t, int64_t, int64_t, int, int, bool, cf*, cf*,
-                                      int64_t, cf*, int64_t, cudaStream_t);
+                                      int64_t, cf*, int64_t, cudaStream_t, long long*);
 
 }  // namespace lg
 }  // namespace mlsb
+
+extern "C" int mlsb_panel_f32(float* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb, float* tau,
+                              float* V, int64_t ldv, float* T, void* stream) {
+  return int(mlsb::lg::panel_factor<float>(M, ld, r0, c0, L, nb, false, tau, V, ldv, T, 0,
+                                           static_cast<cudaStream_t>(stream)));
+}
+extern "C" int mlsb_panel_probe_f32(float* M, int64_t ld, int L, int nb, float* tau, float* V, float* T,
+                                    long long* probe, void* stream) {
+  return int(mlsb::lg::panel_factor<float>(M, ld, 0, 0, L, nb, false, tau, V, L, T, 0,
+                                           static_cast<cudaStream_t>(stream), probe));
+}

@@ -85,6 +85,33 @@ def test_gls_large_size(gpu, port):
     assert not msgs, msgs
 
 
+# several outer WY blocks (NBO = 128 reflectors per trailing update) with a
+# ragged last block and a ragged last panel, in both the RQ and the QR stage
+@pytest.mark.parametrize("shape", [(700, 300, 200), (520, 270, 161), (400, 129, 33)])
+def test_lse_outer_blocks(gpu, port, force_large, shape):
+    m, n, p = shape
+    A, B, b, d = G.lse_problem(m, n, p, 1e4, 1e2, seed=m + p)
+    res, ref, msgs = _lse(gpu, port, A, B, b, d, 1e4 * 10)
+    assert res.trace.status == ref.status == "converged"
+    assert not msgs, msgs
+
+
+@pytest.mark.parametrize("shape", [(600, 260, 400), (300, 140, 290)])
+def test_gls_outer_blocks(gpu, port, force_large, shape):
+    n, m, p = shape
+    W, V, d = G.gls_problem(n, m, p, 1e4, 1e2, seed=n + p)
+    res, ref, msgs = _gls(gpu, port, W, V, d, 1e4 * 10)
+    assert res.trace.status == ref.status == "converged"
+    assert not msgs, msgs
+
+
+def test_complex_gls_outer_blocks(gpu, port):
+    W, V, d = G.gls_problem(330, 150, 270, 1e3, 1e2, seed=33, cplx=True)
+    res, ref, msgs = _gls(gpu, port, W, V, d, 1e3 * 10, cplx=True)
+    assert res.trace.status == ref.status == "converged"
+    assert not msgs, msgs
+
+
 @pytest.mark.parametrize("shape", [(12, 4, 10), (64, 32, 48), (200, 100, 150)])
 def test_complex_gls(gpu, port, shape):
     n, m, p = shape

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <type_traits>
 #include <vector>
 
@@ -229,6 +230,7 @@ struct Blk {
   int L, nbk;
   const FT* T;
   int voff;
+  int ldt;
 };
 // F = P_0 P_1 ... P_last, P_b = I - V_b T_b V_b^H
 template <class FT>
@@ -236,47 +238,84 @@ struct Fac {
   std::vector<Blk<FT>> b;
 };
 
+// ypart: WYB * 256 partials, then WYB values of z, then the ticket counter
 template <class FT, class CT>
 static void apply_F(const Fac<FT>& F, bool herm, CT* x, CT* ypart, cudaStream_t st) {
   const int nb = int(F.b.size());
+  CT* z = ypart + WYB * 256;
+  unsigned* ticket = reinterpret_cast<unsigned*>(z + WYB);
   for (int s = 0; s < nb; ++s) {
     const Blk<FT>& b = F.b[herm ? s : nb - 1 - s];
-    // ~128 CTAs per apply, rows per CTA a multiple of 32
-    int rpc = ((b.L + 127) / 128 + 31) / 32 * 32;
-    if (rpc < 64) rpc = 64;
+    // one 64-row chunk per CTA (several when the block is taller than 256 chunks)
+    const int chunks = (b.L + WYR - 1) / WYR;
+    const int rpc = WYR * ((chunks + 255) / 256);
     const int ncta = (b.L + rpc - 1) / rpc;
-    k_wy_dot<FT, CT><<<ncta, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, x + b.voff, rpc, ypart);
-    k_wy_upd<FT, CT><<<ncta, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, b.T, herm, ypart, ncta, rpc,
-                                          x + b.voff);
+    k_wy_dot<FT, CT><<<ncta, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, x + b.voff, rpc, ypart, b.T, b.ldt, herm,
+                                          ticket, z);
+    k_wy_upd<FT, CT><<<ncta, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, z, rpc, x + b.voff);
   }
 }
 
-// upper-triangular solve with U = M[r0:r0+k, c0:c0+k]; herm: U^H x = b
+// upper-triangular solve with U = M[r0:r0+k, c0:c0+k]; herm: U^H x = b.
+// Diagonal blocks of TRB = 128 (one CTA each), off-diagonal GEMV updates.
 template <class FT, class CT>
 static void trsv(const FT* M, int64_t ld, int64_t r0, int64_t c0, int k, bool herm, CT* x,
                  cudaStream_t st) {
+  const size_t sm = sizeof(FT) * TRB * (TRB + 1) + sizeof(CT) * TRB;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_trsv_diag128<FT, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    attr = true;
+  }
   if (!herm) {
-    for (int i1 = k; i1 > 0; i1 -= 32) {
-      const int i0 = std::max(0, i1 - 32), bs = i1 - i0;
-      k_trsv_diag<FT, CT><<<1, 32, 0, st>>>(M, ld, r0, c0, i0, bs, false, x);
-      if (i0 > 0) k_trsv_off<FT, CT><<<nblk(i0), KT, 0, st>>>(M, ld, r0, c0, i0, bs, k, false, x);
+    for (int i1 = k; i1 > 0; i1 -= TRB) {
+      const int i0 = std::max(0, i1 - TRB), bs = i1 - i0;
+      k_trsv_diag128<FT, CT><<<1, TRB, sm, st>>>(M, ld, r0, c0, i0, bs, false, x);
+      if (i0 > 0) k_trsv_off<FT, CT><<<nblk(i0, 64), KT, 0, st>>>(M, ld, r0, c0, i0, bs, k, false, x);
     }
   } else {
-    for (int i0 = 0; i0 < k; i0 += 32) {
-      const int bs = std::min(32, k - i0);
-      k_trsv_diag<FT, CT><<<1, 32, 0, st>>>(M, ld, r0, c0, i0, bs, true, x);
+    for (int i0 = 0; i0 < k; i0 += TRB) {
+      const int bs = std::min(TRB, k - i0);
+      k_trsv_diag128<FT, CT><<<1, TRB, sm, st>>>(M, ld, r0, c0, i0, bs, true, x);
       if (i0 + bs < k)
         k_trsv_off<FT, CT><<<nblk(k - i0 - bs, KT / 32), KT, 0, st>>>(M, ld, r0, c0, i0, bs, k, true, x);
     }
   }
 }
 
+// column-tiled partials need rows * ceil(cols / GNC) scratch entries; solve()
+// provides the scratch for its thread (without it: one tile, y written directly)
+template <class CT>
+struct GemvScratch {
+  static inline thread_local CT* p = nullptr;
+  static inline thread_local size_t n = 0;
+};
 template <class FT, class CT>
 static void gemv_n(const FT* M, int64_t ld, int r0, int rows, int c0, int cols, Mask mk, const CT* x,
                    CT* y, cudaStream_t st) {
   if (rows <= 0) return;
-  k_gemv_n<FT, CT><<<nblk(rows), KT, 0, st>>>(M, ld, r0, rows, c0, cols, mk, x, y);
+  const int nt = std::max(1, (cols + GNC - 1) / GNC);
+  CT* part = GemvScratch<CT>::p;
+  if (!part || size_t(rows) * nt > GemvScratch<CT>::n) {
+    k_gemv_n<FT, CT><<<dim3((rows + KT - 1) / KT, 1), KT, 0, st>>>(M, ld, r0, rows, c0, cols, std::max(cols, 1),
+                                                                   mk, x, y);
+    return;
+  }
+  k_gemv_n<FT, CT><<<dim3((rows + KT - 1) / KT, nt), KT, 0, st>>>(M, ld, r0, rows, c0, cols, GNC, mk, x, part);
+  k_gemv_n_red<CT><<<nblk(rows), KT, 0, st>>>(part, rows, nt, y);
 }
+template <class CT>
+struct GemvScratchGuard {
+  GemvScratchGuard(CT* p, size_t n) {
+    GemvScratch<CT>::p = p;
+    GemvScratch<CT>::n = n;
+  }
+  ~GemvScratchGuard() {
+    GemvScratch<CT>::p = nullptr;
+    GemvScratch<CT>::n = 0;
+  }
+};
+
 template <class FT, class CT>
 static void gemv_h(const FT* M, int64_t ld, int r0, int rows, int c0, int cols, Mask mk, const CT* x,
                    CT* y, cudaStream_t st) {
@@ -319,7 +358,6 @@ struct Streams {
   cudaEvent_t ev_upd, ev_pan;
   WsBuf ws[2];   // [0] for st, [1] for s2 (inner updates and Gram products)
   void* G;       // NBO x NBO Gram matrix of the block factored on s2
-  void* TB[2];   // merged T of alternating outer blocks, NBO x NBO
 };
 
 // C2 := P^H C2 = C2 - V T^H (V^H C2) for C2 = M[j0:j0+L, c0:c0+nc]
@@ -371,14 +409,14 @@ static cudaError_t block_t(int L, int nbo, const FT* V, const FT* Tp, FT* Tout, 
 // above each panel's unit diagonal); panel j's T at Tbuf + j NB NB.
 template <class FT>
 static cudaError_t qr_stage(FT* M, int64_t ld, int rows, int k, int cend, FT* Vbuf, FT* Tbuf,
-                            FT* taus, Fac<FT>& F, const Streams& S) {
+                            FT* TBig, FT* taus, Fac<FT>& F, const Streams& S) {
   cudaError_t e;
   const int nob = (k + NBO - 1) / NBO;
   if (nob == 0) return cudaSuccess;
   std::vector<size_t> voff(nob + 1, 0);
   for (int B = 0; B < nob; ++B) voff[B + 1] = voff[B] + size_t(rows - B * NBO) * NBO;
   if ((e = cudaMemsetAsync(Vbuf, 0, voff[nob] * sizeof(FT), S.st))) return e;
-  auto TBof = [&](int B) { return static_cast<FT*>(S.TB[B & 1]); };
+  auto TBof = [&](int B) { return TBig + size_t(B) * NBO * NBO; };  // kept for the cascade
   // panels, inner updates and the T merge of block B, on stream s
   auto factor_block = [&](int B, cudaStream_t s, const WsBuf& w) -> cudaError_t {
     const int j0 = B * NBO, nbo = std::min(NBO, k - j0), L0 = rows - j0;
@@ -402,9 +440,7 @@ static cudaError_t qr_stage(FT* M, int64_t ld, int rows, int k, int cend, FT* Vb
     const FT* Tb = nbo > NB ? TBof(B) : Tbuf + size_t(j0 / NB) * NB * NB;
     const int ldt = nbo > NB ? NBO : NB;
     if (B > 0) cudaStreamWaitEvent(S.st, S.ev_pan, 0);  // block B was factored on s2
-    for (int c = j0; c < j0 + nbo; c += NB)
-      F.b.push_back(Blk<FT>{Vb + (c - j0) + int64_t(c - j0) * L0, L0, rows - c, std::min(NB, j0 + nbo - c),
-                            Tbuf + size_t(c / NB) * NB * NB, c});
+    F.b.push_back(Blk<FT>{Vb, L0, L0, nbo, Tb, j0, ldt});
     const int c1 = j0 + nbo;
     if (B + 1 < nob) {
       const int nbn = std::min(NBO, k - c1);
@@ -427,7 +463,7 @@ static cudaError_t qr_stage(FT* M, int64_t ld, int rows, int k, int cend, FT* Vb
 // panels per outer block.
 template <class FT>
 static cudaError_t rq_stage(FT* M, int64_t ld, int rb, int rr, int cb, int cc, FT* Vbuf, FT* Tbuf,
-                            FT* taus, Fac<FT>& F, const Streams& S) {
+                            FT* TBig, FT* taus, Fac<FT>& F, const Streams& S) {
   cudaError_t e;
   const int kk = std::min(rr, cc);
   const int np = (kk + NB - 1) / NB;
@@ -447,7 +483,7 @@ static cudaError_t rq_stage(FT* M, int64_t ld, int rb, int rr, int cb, int cc, F
   std::vector<size_t> voff(nob + 1, 0);
   for (int B = 0; B < nob; ++B) voff[B + 1] = voff[B] + size_t(L_of(B * PPB)) * NBO;
   if ((e = cudaMemsetAsync(Vbuf, 0, voff[nob] * sizeof(FT), S.st))) return e;
-  auto TBof = [&](int B) { return static_cast<FT*>(S.TB[B & 1]); };
+  auto TBof = [&](int B) { return TBig + size_t(B) * NBO * NBO; };  // kept for the cascade
   auto Vp_of = [&](int b) { return Vbuf + voff[b / PPB] + size_t(b % PPB) * NB * L_of((b / PPB) * PPB); };
   auto factor_block = [&](int B, cudaStream_t s, const WsBuf& w) -> cudaError_t {
     const int L0 = L_of(B * PPB), bend = pend(B);
@@ -473,8 +509,7 @@ static cudaError_t rq_stage(FT* M, int64_t ld, int rb, int rr, int cb, int cc, F
     const FT* Vb = Vbuf + voff[B];
     const FT* Tb = nbo > NB ? TBof(B) : Tbuf + size_t(B * PPB) * NB * NB;
     const int ldt = nbo > NB ? NBO : NB;
-    for (int b = B * PPB; b < bend; ++b)
-      F.b.push_back(Blk<FT>{Vp_of(b), L0, L_of(b), nbk_of(b), Tbuf + size_t(b) * NB * NB, 0});
+    F.b.push_back(Blk<FT>{Vb, L0, L0, nbo, Tb, 0, ldt});
     const int above = above_of(bend - 1);
     if (B + 1 < nob) {
       const int nbn = nbo_of(B + 1);
@@ -794,10 +829,11 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   const size_t bytes = sizeof(FT) * (size_t(R) * C + size_t(obz) * R * NBO + size_t(obq) * C * NBO +
                                      size_t(nbz + nbq) * NB * NB + size_t(C + R) + 2 * size_t(L) * NBO +
                                      wn + 8 * size_t(L) + 2 * size_t(NB) * NBO + wn2 +
-                                     3 * size_t(NBO) * NBO) +
+                                     size_t(1 + obz + obq) * NBO * NBO) +
                        sizeof(WT) * (size_t(R) * (6 + ntc) + size_t(C) * (5 + ntr)) +
                        (ext ? 16 * (size_t(ntc) * R + size_t(ntr) * C) + 8 * size_t(R) : 0) +
-                       sizeof(CT) * (10 * size_t(L) + 32 * 256) + 64 * 1024 + 64 * 256;
+                       sizeof(CT) * (10 * size_t(L) + WYB * 256 + WYB + 4) +
+                       (sizeof(CT) + sizeof(FT)) * size_t(L) * ((L + GNC - 1) / GNC) + 64 * 1024 + 64 * 256;
   cudaError_t e = ar.init(bytes + bytes / 4 + (1 << 20), st);
   if (e) return MLSB_ERR_CUDA;
   FT* M = ar.take<FT>(size_t(R) * C);
@@ -814,8 +850,8 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   FT* W2s2 = ar.take<FT>(size_t(NB) * NBO);
   FT* gw2 = ar.take<FT>(wn2);
   FT* Gs2 = ar.take<FT>(size_t(NBO) * NBO);
-  FT* TB0 = ar.take<FT>(size_t(NBO) * NBO);
-  FT* TB1 = ar.take<FT>(size_t(NBO) * NBO);
+  FT* TZb = ar.take<FT>(size_t(obz) * NBO * NBO);  // merged T per outer block
+  FT* TQb = ar.take<FT>(size_t(obq) * NBO * NBO);
   FT* fv[8];
   for (int i = 0; i < 8; ++i) fv[i] = ar.take<FT>(L);
   WT* rinit = ar.take<WT>(R);
@@ -836,7 +872,10 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   double* rlo = ext ? ar.take<double>(R) : nullptr;
   CT* cv[10];
   for (int i = 0; i < 10; ++i) cv[i] = ar.take<CT>(L);
-  CT* ypart = ar.take<CT>(32 * 256);
+  CT* ypart = ar.take<CT>(WYB * 256 + WYB + 4);  // partials | z | ticket
+  const size_t gsn = size_t(L) * ((L + GNC - 1) / GNC);
+  CT* gscr = ar.take<CT>(gsn);
+  FT* gscr_f = ar.take<FT>(gsn);
   char* small = ar.take<char>(64 * 1024);
   if (!small) return MLSB_ERR_CUDA;
   unsigned long long* bits = reinterpret_cast<unsigned long long*>(small);  // [8]
@@ -845,6 +884,10 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   int* flags = reinterpret_cast<int*>(small + 33 * 1024);                    // [8]
   StopOut* so = reinterpret_cast<StopOut*>(small + 34 * 1024);
   cudaMemsetAsync(small, 0, 64 * 1024, st);
+  cudaMemsetAsync(ypart, 0, sizeof(CT) * (WYB * 256 + WYB + 4), st);  // apply tickets start at 0
+  GemvScratchGuard<CT> gsg_c(gscr, gsn);
+  std::unique_ptr<GemvScratchGuard<FT>> gsg_f;
+  if constexpr (!std::is_same<FT, CT>::value) gsg_f.reset(new GemvScratchGuard<FT>(gscr_f, gsn));
 
   const WT* gA = static_cast<const WT*>(P.A);
   const WT* gB = static_cast<const WT*>(P.B);
@@ -937,8 +980,6 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   SS.ws[0] = WsBuf{W, W2, gw, wn};
   SS.ws[1] = WsBuf{Ws2, W2s2, gw2, wn2};
   SS.G = Gs2;
-  SS.TB[0] = TB0;
-  SS.TB[1] = TB1;
   {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -956,11 +997,11 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   } sguard{SS};
   Fac<FT> FZ, FQ;  // QR factor (Z for LSE, Q for GLS) / RQ factor (Q^H for LSE, Z^H for GLS)
   if (lse) {
-    if ((e = rq_stage<FT>(M, ld, m, p, 0, n, VQ, TQ, tauQ, FQ, SS))) return MLSB_ERR_CUDA;
-    if ((e = qr_stage<FT>(M, ld, m, kz, n, VZ, TZ, tauZ, FZ, SS))) return MLSB_ERR_CUDA;
+    if ((e = rq_stage<FT>(M, ld, m, p, 0, n, VQ, TQ, TQb, tauQ, FQ, SS))) return MLSB_ERR_CUDA;
+    if ((e = qr_stage<FT>(M, ld, m, kz, n, VZ, TZ, TZb, tauZ, FZ, SS))) return MLSB_ERR_CUDA;
   } else {
-    if ((e = qr_stage<FT>(M, ld, n, kz, m + p, VZ, TZ, tauZ, FZ, SS))) return MLSB_ERR_CUDA;
-    if ((e = rq_stage<FT>(M, ld, 0, n, m, p, VQ, TQ, tauQ, FQ, SS))) return MLSB_ERR_CUDA;
+    if ((e = qr_stage<FT>(M, ld, n, kz, m + p, VZ, TZ, TZb, tauZ, FZ, SS))) return MLSB_ERR_CUDA;
+    if ((e = rq_stage<FT>(M, ld, 0, n, m, p, VQ, TQ, TQb, tauQ, FQ, SS))) return MLSB_ERR_CUDA;
   }
   // zero pivots in the order of the reference's first failing trsv
   // (LSE: R at lse.hpp:53, then T11 at :60; GLS: T22 at gls.hpp:55, then R at :61)
@@ -1100,7 +1141,18 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
     }
   }
   out->inner = 0;
+  // MLSB_LOOP_PROF=1: CUDA-event split of the first refinement pass (stderr)
+  static const bool loop_prof = getenv("MLSB_LOOP_PROF") != nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> pev;
+  auto mark = [&](const char* name) {
+    if (!loop_prof || pass != 1) return;
+    cudaEvent_t e2;
+    cudaEventCreate(&e2);
+    cudaEventRecord(e2, st);
+    pev.emplace_back(name, e2);
+  };
   for (pass = 1; pass <= P.maxit; ++pass) {
+    mark("start");
     // row initialisers and weights of this pass
     if (lse) {
       k_sub<WT><<<nblk(m), KT, 0, st>>>(rinit, sw, m, rrow);                  // b - r
@@ -1135,6 +1187,7 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       k_resid_reduce<WT><<<nblk(R + C), KT, 0, st>>>(R, C, ntc, ntr, rpart, cpart, rrow, cinit, rout,
                                                      cout);
     }
+    mark("residual");
     StopIn si{};
     if (lse) {  // f1, f2, f3 | r, v, x
       si.seg[0] = rout;       si.len[0] = m;
@@ -1160,6 +1213,7 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       --pass;
       break;
     }
+    mark("stop+sync");
     const double g1 = hso.nrm[0], g2n = hso.nrm[1], g3 = hso.nrm[2];
     const double s3 = hso.nrm[3], s4 = hso.nrm[4], s5 = hso.nrm[5];
     double d1, d2, d3;
@@ -1220,25 +1274,37 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       k_demote<WT, CT><<<nblk(n), KT, 0, st>>>(cout, n, sb, u);
       k_demote<WT, CT><<<nblk(m), KT, 0, st>>>(rout, m, sb, w);
       k_demote<WT, CT><<<nblk(p), KT, 0, st>>>(rout + m, p, sb, y2);
+      mark("demote");
       apply_F<FT, CT>(FQ, true, u, ypart, st);                  // u = Q f3 = F^H f3
+      mark("applyQ");
       apply_F<FT, CT>(FZ, true, w, ypart, st);                  // w = Z^H f1
+      mark("applyZ");
       trsv<FT, CT>(M, ld, m, n - p, p, false, y2, st);          // R y2 = f2
+      mark("trsvR");
       k_copy<CT><<<nblk(k), KT, 0, st>>>(u, k, q1);
       trsv<FT, CT>(M, ld, 0, 0, k, true, q1, st);               // T11^H q1 = u1
+      mark("trsvT11h");
       gemv_n<FT, CT>(M, ld, 0, k, k, p, none, y2, t4, st);       // T12 y2
       gemv_n<FT, CT>(M, ld, k, m - k, k, p, Mask{1, 0, 0}, y2, t4 + k, st);  // T22 y2
+      mark("gemv_n x2");
       k_subsub<CT><<<nblk(k), KT, 0, st>>>(w, q1, t4, k, y);      // y1 rhs = w1 - q1 - T12 y2
       k_copy<CT><<<nblk(k), KT, 0, st>>>(q1, k, w);               // q = [q1; w2 - T22 y2]
       k_sub<CT><<<nblk(m - k), KT, 0, st>>>(w + k, t4 + k, m - k, w + k);
       k_copy<CT><<<nblk(m), KT, 0, st>>>(w, m, dr);
       k_copy<CT><<<nblk(p), KT, 0, st>>>(y2, p, y + k);
+      mark("elementwise");
       trsv<FT, CT>(M, ld, 0, 0, k, false, y, st);               // T11 y1 = ...
+      mark("trsvT11");
       apply_F<FT, CT>(FQ, false, y, ypart, st);                 // dx = Q^H y = F y
+      mark("applyQh");
       apply_F<FT, CT>(FZ, false, dr, ypart, st);                // dr = Z q = F q
+      mark("applyZh");
       gemv_h<FT, CT>(M, ld, 0, k, k, p, none, w, t4, st);        // T12^H q1
       gemv_h<FT, CT>(M, ld, k, m - k, k, p, Mask{1, 0, 0}, w + k, tq, st);  // T22^H q2
+      mark("gemv_h x2");
       k_addsub<CT><<<nblk(p), KT, 0, st>>>(t4, tq, u + k, p, t4);  // s = T12^H q1 + (T22^H q2 - u2)
       trsv<FT, CT>(M, ld, m, n - p, p, true, t4, st);            // R^H dv = s
+      mark("trsvRh");
       k_promote_add<WT, CT><<<nblk(m), KT, 0, st>>>(sw, m, dr, sb, false, flags + 3);
       k_promote_add<WT, CT><<<nblk(p), KT, 0, st>>>(sw + m, p, t4, sb, false, flags + 3);
       k_promote_add<WT, CT><<<nblk(n), KT, 0, st>>>(su, n, y, sb, false, flags + 3);
@@ -1276,6 +1342,17 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       k_promote_add<WT, CT><<<nblk(n), KT, 0, st>>>(sw, n, u, sb, true, flags + 3);  // dz = -Q h
     }
     if ((e = cudaGetLastError())) return MLSB_ERR_CUDA;
+    mark("update");
+    if (loop_prof && pass == 1) {
+      cudaStreamSynchronize(st);
+      for (size_t i = 1; i < pev.size(); ++i) {
+        float ms2 = 0.f;
+        cudaEventElapsedTime(&ms2, pev[i - 1].second, pev[i].second);
+        fprintf(stderr, "[loop] %-12s %8.3f ms\n", pev[i].first, ms2);
+      }
+      for (auto& pe : pev) cudaEventDestroy(pe.second);
+      pev.clear();
+    }
   }
   if (pass > P.maxit) pass = P.maxit;
   if (status == 1) {

@@ -494,12 +494,18 @@ __global__ void __launch_bounds__(256) k_tmerge(int nbo, const T* __restrict__ G
     S[r + c * LDS] = br == bc ? Tp[br * NB * NB + (r - br * NB) + (c - bc * NB) * NB] : zero<T>();
   }
   __syncthreads();
+  T* GX = X + NBO * NB;  // staged block column G[0:h, c0:c0+w]
   for (int j = 1; j < nblk; ++j) {
     const int c0 = j * NB, w = min(NB, nbo - c0), h = c0;
     for (int e = tid; e < h * w; e += 256) {
       const int r = e % h, c = e / h;
+      GX[r + c * NBO] = G[r + int64_t(c0 + c) * ldg];
+    }
+    __syncthreads();
+    for (int e = tid; e < h * w; e += 256) {
+      const int r = e % h, c = e / h;
       T acc = zero<T>();
-      for (int t = 0; t <= c; ++t) mac(acc, G[r + int64_t(c0 + t) * ldg], S[(c0 + t) + (c0 + c) * LDS]);
+      for (int t = 0; t <= c; ++t) mac(acc, GX[r + t * NBO], S[(c0 + t) + (c0 + c) * LDS]);
       X[r + c * NBO] = acc;
     }
     __syncthreads();
@@ -521,7 +527,7 @@ template <class T>
 static cudaError_t tmerge_t(int nbo, const T* G, int ldg, const T* Tp, T* Tout, int ldt,
                             cudaStream_t st) {
   if (nbo <= 0 || nbo > NBO) return cudaErrorInvalidValue;
-  const size_t sm = sizeof(T) * (size_t(NBO) * (NBO + 1) + size_t(NBO) * NB);
+  const size_t sm = sizeof(T) * (size_t(NBO) * (NBO + 1) + 2 * size_t(NBO) * NB);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_tmerge<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));

@@ -277,6 +277,11 @@ __device__ __forceinline__ void st_async(uint32_t a, float v, uint32_t bar) {
                "r"(bar)
                : "memory");
 }
+__device__ __forceinline__ void st_async(uint32_t a, float4 v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(a),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(bar)
+               : "memory");
+}
 __device__ __forceinline__ void st_async(uint32_t a, double v, uint32_t bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(a), "d"(v),
                "r"(bar)
@@ -301,9 +306,10 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelArgs<float> a) {
   constexpr int NW = NT / 32;
   __shared__ float wpart[NW][NB];
   __shared__ double wnorm[NW];
-  __shared__ float prow_s[NB];
-  __shared__ float xd[2][PCL][2 * NB];  // [parity][rank][d | pivot row]
-  __shared__ double xn[2][PCL];
+  __shared__ __align__(16) float prow_s[NB];
+  __shared__ __align__(16) float xd[2][PCL][NB];  // [parity][rank] CTA partials of d
+  __shared__ __align__(16) float xp[2][NB];       // [parity] pivot row (from its owner CTA)
+  __shared__ double xn[2][PCL];                   // [parity][rank] CTA partials of ||x||^2
   __shared__ __align__(8) unsigned long long xbar[2];  // exchange arrivals, per parity
   __shared__ uint32_t rbase[PCL];                      // cluster address of xd in CTA c
   __shared__ __align__(16) float coef_s[NB];
@@ -336,161 +342,171 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelArgs<float> a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster_barrier();  // every exchange barrier initialised before any remote signal
-  const uint32_t xbytes = uint32_t(ncl) * (2 * NB * sizeof(float) + sizeof(double));
-  // my slot in the exchange buffers and the barrier, as offsets from xd (same in every CTA)
-  const uint32_t off_slot = (tid < 2 * NB ? uint32_t(__cvta_generic_to_shared(&xd[0][rank][tid]))
-                                          : uint32_t(__cvta_generic_to_shared(&xn[0][rank]))) - xd0;
+  const uint32_t xbytes = uint32_t(ncl) * (NB * sizeof(float) + sizeof(double)) + NB * sizeof(float);
+  // exchange buffers and barrier as offsets from xd (the same in every CTA)
+  const uint32_t off_d = uint32_t(__cvta_generic_to_shared(&xd[0][rank][0])) - xd0;
+  const uint32_t off_p = uint32_t(__cvta_generic_to_shared(&xp[0][0])) - xd0;
+  const uint32_t off_n = uint32_t(__cvta_generic_to_shared(&xn[0][rank])) - xd0;
   const uint32_t off_bar = uint32_t(__cvta_generic_to_shared(&xbar[0])) - xd0;
-  constexpr uint32_t par_d = sizeof(xd[0]), par_n = sizeof(xn[0]);
+  constexpr uint32_t par_d = sizeof(xd[0]), par_p = sizeof(xp[0]), par_n = sizeof(xn[0]);
 
+  // Rotating frame: at step q, P[i][f] holds column (q + f) mod NB, so the
+  // current column is always P[i][0] and the step is the same code for every
+  // q (a real loop: the unrolled 32-step body does not fit the i-cache).
+#pragma unroll 1
+  for (int q = 0; q < nb; ++q) {
+    const int par = q & 1;
+    long long* pq = (a.probe && rank == 0 && tid == 0) ? a.probe + 8 * q : nullptr;
+    if (pq) pq[0] = clock64();
+    // ---- 1. thread partials (frame order)
+    float d[NB];
 #pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    if (q < nb) {  // uniform over the cluster
-      const int par = q & 1;
-      long long* pq = (a.probe && rank == 0 && tid == 0) ? a.probe + 8 * q : nullptr;
-      if (pq) pq[0] = clock64();
-      // ---- 1. thread partials
-      float d[NB];
+    for (int f = 0; f < NB; ++f) d[f] = 0.f;
+    double nn = 0.0;
 #pragma unroll
-      for (int k = 0; k < NB; ++k) d[k] = 0.f;
-      double nn = 0.0;
+    for (int i = 0; i < RPT; ++i) {
+      if (row[i] > q) {
+        const float x = P[i][0];
+        nn = fma(double(x), double(x), nn);
 #pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        if (row[i] > q) {
-          const float x = P[i][q];
-          nn = fma(double(x), double(x), nn);
+        for (int f = 0; f < NB; ++f) d[f] = fmaf(x, P[i][f], d[f]);
+      } else if (row[i] == q) {
 #pragma unroll
-          for (int k = 0; k < NB; ++k) d[k] = fmaf(x, P[i][k], d[k]);
-        } else if (row[i] == q) {
-#pragma unroll
-          for (int k = 0; k < NB; ++k) prow_s[k] = P[i][k];
-        }
+        for (int f = 0; f < NB; ++f) prow_s[f] = P[i][f];
       }
-      // ---- 2. warp transposed reduction: lane l ends with the warp sum of d[l]
-#pragma unroll
-      for (int s = 16; s >= 1; s >>= 1) {
-        const bool up = (l & s) != 0;
-#pragma unroll
-        for (int j = 0; j < s; ++j) {
-          const float send = up ? d[j] : d[j + s];
-          const float keep = up ? d[j + s] : d[j];
-          d[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-        }
-      }
-      nn = wsum(nn);
-      wpart[w][l] = d[0];
-      if (l == 0) wnorm[w] = nn;
-      if (pq) pq[1] = clock64();
-      __syncthreads();
-      if (pq) pq[2] = clock64();
-      // ---- 3. CTA partials pushed into slot [rank] of every CTA's exchange
-      //         buffer by st.async, each landing store counted on the
-      //         destination's mbarrier (no fence, no cluster barrier)
-      if (tid == 0)
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                         uint32_t(__cvta_generic_to_shared(&xbar[par]))),
-                     "r"(xbytes)
-                     : "memory");
-      if (tid <= 2 * NB) {
-        const uint32_t so = off_slot + (tid < 2 * NB ? par * par_d : par * par_n), bo = off_bar + 8 * par;
-        if (tid < 2 * NB) {
-          float v;
-          if (tid < NB) {
-            float t[NW];
-#pragma unroll
-            for (int ww = 0; ww < NW; ++ww) t[ww] = wpart[ww][tid];
-            v = 0.f;
-#pragma unroll
-            for (int ww = 0; ww < NW; ++ww) v += t[ww];
-          } else {
-            v = (q >= rb && q < re) ? prow_s[tid - NB] : 0.f;
-          }
-#pragma unroll
-          for (int c = 0; c < PCL; ++c)
-            if (c < ncl) st_async(rbase[c] + so, v, rbase[c] + bo);
-        } else {
-          double t[NW];
-#pragma unroll
-          for (int ww = 0; ww < NW; ++ww) t[ww] = wnorm[ww];
-          double v = 0.0;
-#pragma unroll
-          for (int ww = 0; ww < NW; ++ww) v += t[ww];
-#pragma unroll
-          for (int c = 0; c < PCL; ++c)
-            if (c < ncl) st_async(rbase[c] + so, v, rbase[c] + bo);
-        }
-      }
-      // ---- 4. warp 0: totals in rank order (lane k: d_k, p_k), xLARFG, the
-      //         update coefficients coef_k = tau v^T P[:, k] and Gram entries
-      if (pq) pq[3] = clock64();
-      if (w == 0) {
-        mbar_wait(&xbar[par], (q >> 1) & 1);
-        if (pq) pq[4] = clock64();
-        float td[PCL], tp[PCL];
-        double tn[PCL];
-#pragma unroll
-        for (int c = 0; c < PCL; ++c) {
-          const bool in = c < ncl;
-          td[c] = in ? xd[par][c][l] : 0.f;
-          tp[c] = in ? xd[par][c][NB + l] : 0.f;
-          tn[c] = in ? xn[par][c] : 0.0;
-        }
-        float dk = 0.f, pk = 0.f;
-        double nrm = 0.0;
-#pragma unroll
-        for (int c = 0; c < PCL; ++c) {
-          dk += td[c];
-          pk += tp[c];
-          nrm += tn[c];
-        }
-        float tau, inv, beta;
-        larfg_s(__shfl_sync(0xffffffffu, pk, q), nrm, tau, inv, beta);
-        coef_s[l] = l > q ? tau * fmaf(inv, dk, pk) : 0.f;
-        if (l < q) G[l + NB * q] = fmaf(inv, dk, pk);  // v_l^T v_q
-        if (l == 0) {
-          scal[0] = inv;
-          scal[1] = beta;
-          taus[q] = tau;
-        }
-      }
-      if (pq) pq[5] = clock64();
-      __syncthreads();
-      if (pq) pq[6] = clock64();
-      // ---- 5. rank-1 update of my rows, in registers
-      const float inv = scal[0], beta = scal[1];
-      float v[RPT];
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) v[i] = row[i] == q ? 1.f : (row[i] > q ? inv * P[i][q] : 0.f);
-#pragma unroll
-      for (int k4 = 0; k4 < NB; k4 += 4) {
-        if (k4 + 3 > q) {
-          const float4 c4 = *reinterpret_cast<const float4*>(&coef_s[k4]);
-          const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            if (k4 + t > q)
-#pragma unroll
-              for (int i = 0; i < RPT; ++i) P[i][k4 + t] = fmaf(-cc[t], v[i], P[i][k4 + t]);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < RPT; ++i)
-        if (row[i] >= q) P[i][q] = row[i] == q ? beta : v[i];
-      if (pq) pq[7] = clock64();
     }
+    // ---- 2. warp transposed reduction: lane l ends with the warp sum of d[l]
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const bool up = (l & s) != 0;
+#pragma unroll
+      for (int j = 0; j < s; ++j) {
+        const float send = up ? d[j] : d[j + s];
+        const float keep = up ? d[j + s] : d[j];
+        d[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+      }
+    }
+    nn = wsum(nn);
+    wpart[w][l] = d[0];
+    if (l == 0) wnorm[w] = nn;
+    if (pq) pq[1] = clock64();
+    __syncthreads();
+    if (pq) pq[2] = clock64();
+    // ---- 3. CTA partials pushed into slot [rank] of every CTA's exchange
+    //         buffer by st.async, each landing store counted on the
+    //         destination's mbarrier (no fence, no cluster barrier)
+    if (tid == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       uint32_t(__cvta_generic_to_shared(&xbar[par]))),
+                   "r"(xbytes)
+                   : "memory");
+    {
+      // one 16-byte chunk per (destination, chunk) pair: threads u = 8 c + j
+      const uint32_t bo = off_bar + 8 * par;
+      for (int u = tid; u < 8 * ncl; u += NT) {
+        const int c = u >> 3, j = u & 7;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) {
+          const float4 t = *reinterpret_cast<const float4*>(&wpart[ww][4 * j]);
+          v.x += t.x, v.y += t.y, v.z += t.z, v.w += t.w;
+        }
+        st_async(rbase[c] + off_d + par * par_d + 16 * j, v, rbase[c] + bo);
+      }
+      if (q >= rb && q < re)  // this CTA owns the pivot row
+        for (int u = tid; u < 8 * ncl; u += NT) {
+          const int c = u >> 3, j = u & 7;
+          st_async(rbase[c] + off_p + par * par_p + 16 * j, *reinterpret_cast<const float4*>(&prow_s[4 * j]),
+                   rbase[c] + bo);
+        }
+      if (tid < ncl) {
+        double t[NW];
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) t[ww] = wnorm[ww];
+        double v = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) v += t[ww];
+        st_async(rbase[tid] + off_n + par * par_n, v, rbase[tid] + bo);
+      }
+    }
+    // ---- 4. warp 0: totals in rank order (lane f: d_f, p_f), xLARFG, the
+    //         update coefficients coef_f = tau v^T P[:, f] and Gram entries
+    if (pq) pq[3] = clock64();
+    if (w == 0) {
+      mbar_wait(&xbar[par], (q >> 1) & 1);
+      if (pq) pq[4] = clock64();
+      float td[PCL];
+      double tn[PCL];
+#pragma unroll
+      for (int c = 0; c < PCL; ++c) {
+        const bool in = c < ncl;
+        td[c] = in ? xd[par][c][l] : 0.f;
+        tn[c] = in ? xn[par][c] : 0.0;
+      }
+      const float pk = xp[par][l];
+      // fixed pairwise tree over the ranks (absent ranks add exact zeros)
+#pragma unroll
+      for (int h = PCL / 2; h >= 1; h >>= 1)
+#pragma unroll
+        for (int c = 0; c < h; ++c) {
+          td[c] += td[c + h];
+          tn[c] += tn[c + h];
+        }
+      const float dk = td[0];
+      const double nrm = tn[0];
+      float tau, inv, beta;
+      larfg_s(__shfl_sync(0xffffffffu, pk, 0), nrm, tau, inv, beta);
+      const float s = fmaf(inv, dk, pk);  // v^T P[:, f]
+      coef_s[l] = (l >= 1 && l < nb - q) ? tau * s : 0.f;
+      if (l >= NB - q) G[(q + l - NB) + NB * q] = s;  // v_k^T v_q, k = q + l - NB < q
+      if (l == 0) {
+        scal[0] = inv;
+        scal[1] = beta;
+        taus[q] = tau;
+      }
+    }
+    if (pq) pq[5] = clock64();
+    __syncthreads();
+    if (pq) pq[6] = clock64();
+    // ---- 5. rank-1 update of my rows, in registers, then rotate the frame
+    const float inv = scal[0], beta = scal[1];
+    float v[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) v[i] = row[i] == q ? 1.f : (row[i] > q ? inv * P[i][0] : 0.f);
+#pragma unroll
+    for (int f4 = 0; f4 < NB; f4 += 4) {
+      const float4 c4 = *reinterpret_cast<const float4*>(&coef_s[f4]);
+      const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (f4 + t >= 1)
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) P[i][f4 + t] = fmaf(-cc[t], v[i], P[i][f4 + t]);
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const float p0 = row[i] == q ? beta : (row[i] > q ? v[i] : P[i][0]);
+#pragma unroll
+      for (int f = 0; f < NB - 1; ++f) P[i][f] = P[i][f + 1];
+      P[i][NB - 1] = p0;
+    }
+    if (pq) pq[7] = clock64();
   }
   __syncthreads();
-  // ---- write back the factored panel and the dense reflector block
+  // ---- write back the factored panel and the dense reflector block; frame
+  //      index f holds column (nb + f) mod NB after nb steps
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     const int r = row[i];
     if (r < 0) continue;
     const int64_t vi = a.rq ? (a.c0 - r - a.vbase) : r;
 #pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      if (k >= nb) break;
-      st_view(a, r, k, P[i][k]);
-      a.V[vi + k * a.ldv] = r < k ? 0.f : (r == k ? 1.f : P[i][k]);
+    for (int f = 0; f < NB; ++f) {
+      const int k = (nb + f) & (NB - 1);
+      if (k < nb) {
+        st_view(a, r, k, P[i][f]);
+        a.V[vi + k * a.ldv] = r < k ? 0.f : (r == k ? 1.f : P[i][f]);
+      }
     }
   }
   if (rank == 0) {

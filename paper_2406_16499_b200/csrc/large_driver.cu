@@ -238,21 +238,18 @@ struct Fac {
   std::vector<Blk<FT>> b;
 };
 
-// ypart: WYB * 256 partials, then WYB values of z, then the ticket counter
+// ypart: WYB * 256 partials of the dot kernel
 template <class FT, class CT>
 static void apply_F(const Fac<FT>& F, bool herm, CT* x, CT* ypart, cudaStream_t st) {
   const int nb = int(F.b.size());
-  CT* z = ypart + WYB * 256;
-  unsigned* ticket = reinterpret_cast<unsigned*>(z + WYB);
   for (int s = 0; s < nb; ++s) {
     const Blk<FT>& b = F.b[herm ? s : nb - 1 - s];
-    // one 64-row chunk per CTA (several when the block is taller than 256 chunks)
-    const int chunks = (b.L + WYR - 1) / WYR;
-    const int rpc = WYR * ((chunks + 255) / 256);
-    const int ncta = (b.L + rpc - 1) / rpc;
-    k_wy_dot<FT, CT><<<ncta, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, x + b.voff, rpc, ypart, b.T, b.ldt, herm,
-                                          ticket, z);
-    k_wy_upd<FT, CT><<<ncta, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, z, rpc, x + b.voff);
+    const int dch = (b.L + WYD - 1) / WYD, dpc = WYD * ((dch + 255) / 256);  // <= 256 partials
+    const int nd = (b.L + dpc - 1) / dpc;
+    const int uch = (b.L + WYR - 1) / WYR, upc = WYR * ((uch + 147) / 148);  // <= 148 update CTAs
+    const int nu = (b.L + upc - 1) / upc;
+    k_wy_dot<FT, CT><<<nd, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, x + b.voff, dpc, ypart);
+    k_wy_upd<FT, CT><<<nu, KT, 0, st>>>(b.V, b.ldv, b.L, b.nbk, ypart, nd, b.T, b.ldt, herm, upc, x + b.voff);
   }
 }
 

@@ -1057,7 +1057,8 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
         }
       }
       if (!ext) {
-        k_resid_tile<WT><<<g2, KT, 0, st>>>(S, m, n, gvec, sw, rpart, cpart);
+        if constexpr (tr<WT>::cplx) k_resid_tile<WT><<<g2, KT, 0, st>>>(S, m, n, gvec, sw, rpart, cpart);  // complex128: register budget
+      else k_resid_stream<WT><<<g2, KT, 0, st>>>(S, m, n, gvec, sw, rpart, cpart);
         k_resid_reduce<WT><<<nblk(m + n), KT, 0, st>>>(m, n, ntc, (m + RTR - 1) / RTR, rpart, cpart,
                                                        rinit, nullptr, rout, cout);
       }
@@ -1180,7 +1181,8 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       }
     }
     if (!ext) {
-      k_resid_tile<WT><<<g2, KT, 0, st>>>(S, R, C, su, wvec, rpart, cpart);
+      if constexpr (tr<WT>::cplx) k_resid_tile<WT><<<g2, KT, 0, st>>>(S, R, C, su, wvec, rpart, cpart);  // complex128: register budget
+      else k_resid_stream<WT><<<g2, KT, 0, st>>>(S, R, C, su, wvec, rpart, cpart);
       k_resid_reduce<WT><<<nblk(R + C), KT, 0, st>>>(R, C, ntc, ntr, rpart, cpart, rrow, cinit, rout,
                                                      cout);
     }

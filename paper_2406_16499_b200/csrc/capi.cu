@@ -120,13 +120,13 @@ Shape gls_shape(int64_t n, int64_t m, int64_t p) {
 // or the whole-GPU large path (blocked GRQ/GQR + host-driven IR).
 bool route_large(const Shape& s, const mlsb_config* cfg, bool cplx) {
   if (cplx) return true;
-  if (getenv("MLSB_FORCE_LARGE") && cfg->u_f == MLSB_LOW) return true;
+  if (getenv("MLSB_FORCE_LARGE")) return true;
   const size_t lim = mlsb::device_smem_limit();
   if (s.kind == mlsb::KIND_LSE && mlsb::lse_reg_supported(s.m, s.n, s.p, cfg->u_f, cfg->u_s, cfg->u_r, lim))
     return false;
   const int64_t R = s.kind == mlsb::KIND_LSE ? s.m + s.p : s.n;
   const int64_t C = s.kind == mlsb::KIND_LSE ? s.n : s.m + s.p;
-  const bool large_ok = cfg->u_f == MLSB_LOW;  // (u_r = extended: real problems)
+  const bool large_ok = true;  // any real precision combination (u_f = working: binary64 panels/GEMMs)
   const size_t need_g = mlsb::tile_smem_bytes(s.kind, s.m, s.n, s.p, cfg->u_f, cfg->u_s, cfg->u_r, true);
   if (need_g > lim) return large_ok;
   return large_ok && R * C > 384 * 384;

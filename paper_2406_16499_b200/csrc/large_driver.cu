@@ -327,6 +327,8 @@ static cudaError_t gemm(bool ha, bool hb, int Mr, int N, int K, double alpha, co
   if constexpr (tr<FT>::cplx)
     return gemm_c64(ha, hb, Mr, N, K, cf{float(alpha), 0.f}, A, lda, B, ldb, cf{float(beta), 0.f}, C,
                     ldc, work, wn, st);
+  else if constexpr (std::is_same<FT, double>::value)
+    return gemm_f64(ha, hb, Mr, N, K, alpha, A, lda, B, ldb, beta, C, ldc, work, wn, st);
   else
     return gemm_f32(ha, hb, Mr, N, K, float(alpha), A, lda, B, ldb, float(beta), C, ldc, work, wn, st);
 }
@@ -356,6 +358,11 @@ struct Streams {
   WsBuf ws[2];   // [0] for st, [1] for s2 (inner updates and Gram products)
   void* G;       // NBO x NBO Gram matrix of the block factored on s2
 };
+
+// resident-CTA cap of a trailing update that runs beside a look-ahead block
+// factorization: 148 + 100 CTAs of the 2-per-SM GEMM tile leave one slot free
+// on 48 SMs for the panel cluster and the small inner-update GEMMs
+constexpr int kTrailCap = 148 + 100;
 
 // C2 := P^H C2 = C2 - V T^H (V^H C2) for C2 = M[j0:j0+L, c0:c0+nc]
 template <class FT>
@@ -398,6 +405,7 @@ static cudaError_t block_t(int L, int nbo, const FT* V, const FT* Tp, FT* Tout, 
                     st)))
     return e;
   if constexpr (tr<FT>::cplx) return tmerge_c64(nbo, G, nbo, Tp, Tout, NBO, st);
+  else if constexpr (std::is_same<FT, double>::value) return tmerge_f64(nbo, G, nbo, Tp, Tout, NBO, st);
   else return tmerge_f32(nbo, G, nbo, Tp, Tout, NBO, st);
 }
 
@@ -415,6 +423,16 @@ static cudaError_t qr_stage(FT* M, int64_t ld, int rows, int k, int cend, FT* Vb
   if ((e = cudaMemsetAsync(Vbuf, 0, voff[nob] * sizeof(FT), S.st))) return e;
   auto TBof = [&](int B) { return TBig + size_t(B) * NBO * NBO; };  // kept for the cascade
   // panels, inner updates and the T merge of block B, on stream s
+  // MLSB_FACT_PROF=1: split of the block factorizations (panels | inner updates | T merge)
+  static const bool bprof = getenv("MLSB_FACT_PROF") != nullptr;
+  std::vector<cudaEvent_t> be;
+  auto bmark = [&](cudaStream_t s2) {
+    if (!bprof) return;
+    cudaEvent_t x;
+    cudaEventCreate(&x);
+    cudaEventRecord(x, s2);
+    be.push_back(x);
+  };
   auto factor_block = [&](int B, cudaStream_t s, const WsBuf& w) -> cudaError_t {
     const int j0 = B * NBO, nbo = std::min(NBO, k - j0), L0 = rows - j0;
     FT* Vb = Vbuf + voff[B];
@@ -423,14 +441,28 @@ static cudaError_t qr_stage(FT* M, int64_t ld, int rows, int k, int cend, FT* Vb
       const int nbk = std::min(NB, j0 + nbo - c), o = c - j0;
       FT* Vp = Vb + o + int64_t(o) * L0;
       FT* Tp = Tbuf + size_t(c / NB) * NB * NB;
+      bmark(s);
       if ((e2 = panel_factor<FT>(M, ld, c, c, rows - c, nbk, false, taus + c, Vp, L0, Tp, 0, s))) return e2;
+      bmark(s);
       if ((e2 = qr_update<FT>(M, ld, c, rows - c, nbk, c + nbk, j0 + nbo - c - nbk, Vp, L0, Tp, NB, w, s)))
         return e2;
     }
-    if (nbo > NB) return block_t<FT>(L0, nbo, Vb, Tbuf + size_t(j0 / NB) * NB * NB, TBof(B), S, s);
+    bmark(s);
+    if (nbo > NB && (e2 = block_t<FT>(L0, nbo, Vb, Tbuf + size_t(j0 / NB) * NB * NB, TBof(B), S, s))) return e2;
+    bmark(s);
     return cudaSuccess;
   };
   if ((e = factor_block(0, S.st, S.ws[0]))) return e;
+  // MLSB_FACT_PROF=1: per-block event split of the look-ahead pipeline (stderr)
+  static const bool fprof = getenv("MLSB_FACT_PROF") != nullptr;
+  std::vector<cudaEvent_t> fe;
+  auto fmark = [&](cudaStream_t s) {
+    if (!fprof) return;
+    cudaEvent_t x;
+    cudaEventCreate(&x);
+    cudaEventRecord(x, s);
+    fe.push_back(x);
+  };
   for (int B = 0; B < nob; ++B) {
     const int j0 = B * NBO, nbo = std::min(NBO, k - j0), L0 = rows - j0;
     const FT* Vb = Vbuf + voff[B];
@@ -441,16 +473,53 @@ static cudaError_t qr_stage(FT* M, int64_t ld, int rows, int k, int cend, FT* Vb
     const int c1 = j0 + nbo;
     if (B + 1 < nob) {
       const int nbn = std::min(NBO, k - c1);
+      fmark(S.st);
       if ((e = qr_update<FT>(M, ld, j0, L0, nbo, c1, nbn, Vb, L0, Tb, ldt, S.ws[0], S.st))) return e;
       cudaEventRecord(S.ev_upd, S.st);
+      fmark(S.st);
       cudaStreamWaitEvent(S.s2, S.ev_upd, 0);
       if ((e = factor_block(B + 1, S.s2, S.ws[1]))) return e;
       cudaEventRecord(S.ev_pan, S.s2);
-      if ((e = qr_update<FT>(M, ld, j0, L0, nbo, c1 + nbn, cend - c1 - nbn, Vb, L0, Tb, ldt, S.ws[0], S.st)))
-        return e;
+      fmark(S.s2);
+      set_gemm_cta_cap(kTrailCap);  // leave SM slots to the look-ahead stream
+      e = qr_update<FT>(M, ld, j0, L0, nbo, c1 + nbn, cend - c1 - nbn, Vb, L0, Tb, ldt, S.ws[0], S.st);
+      set_gemm_cta_cap(0);
+      if (e) return e;
+      fmark(S.st);
     } else {
       if ((e = qr_update<FT>(M, ld, j0, L0, nbo, c1, cend - c1, Vb, L0, Tb, ldt, S.ws[0], S.st))) return e;
     }
+  }
+  if (fprof && !fe.empty()) {
+    cudaEventSynchronize(fe.back());
+    double tn = 0, tf = 0, tt = 0;
+    for (size_t i = 0; i + 3 < fe.size(); i += 4) {
+      float a = 0, b = 0, c = 0;
+      cudaEventElapsedTime(&a, fe[i], fe[i + 1]);
+      cudaEventElapsedTime(&b, fe[i + 1], fe[i + 2]);
+      cudaEventElapsedTime(&c, fe[i + 1], fe[i + 3]);
+      tn += a, tf += b, tt += c;
+    }
+    float wall = 0;
+    cudaEventElapsedTime(&wall, fe.front(), fe.back());
+    fprintf(stderr, "[fact] qr_stage rows %d k %d: next-cols updates %.3f ms, block factorizations %.3f ms, "
+                    "trailing updates %.3f ms, wall %.3f ms\n", rows, k, tn, tf, tt, wall);
+    // per block: 4 x (panel, inner update) then T merge = 10 marks
+    double tp = 0, ti = 0, tm = 0;
+    for (size_t i = 0; i + 9 < be.size(); i += 10) {
+      for (int q = 0; q < 4; ++q) {
+        float a2 = 0, b2 = 0;
+        cudaEventElapsedTime(&a2, be[i + 2 * q], be[i + 2 * q + 1]);
+        cudaEventElapsedTime(&b2, be[i + 2 * q + 1], be[i + 2 * q + 2]);
+        tp += a2, ti += b2;
+      }
+      float c2 = 0;
+      cudaEventElapsedTime(&c2, be[i + 8], be[i + 9]);
+      tm += c2;
+    }
+    fprintf(stderr, "[fact]   blocks: panels %.3f ms, inner updates %.3f ms, Gram + T merge %.3f ms\n", tp, ti, tm);
+    for (auto x : be) cudaEventDestroy(x);
+    for (auto x : fe) cudaEventDestroy(x);
   }
   return cudaSuccess;
 }
@@ -515,7 +584,10 @@ static cudaError_t rq_stage(FT* M, int64_t ld, int rb, int rr, int cb, int cc, F
       cudaStreamWaitEvent(S.s2, S.ev_upd, 0);
       if ((e = factor_block(B + 1, S.s2, S.ws[1]))) return e;
       cudaEventRecord(S.ev_pan, S.s2);
-      if ((e = rq_update<FT>(M, ld, 0, above - nbn, cb, L0, nbo, Vb, L0, Tb, ldt, S.ws[0], S.st))) return e;
+      set_gemm_cta_cap(kTrailCap);
+      e = rq_update<FT>(M, ld, 0, above - nbn, cb, L0, nbo, Vb, L0, Tb, ldt, S.ws[0], S.st);
+      set_gemm_cta_cap(0);
+      if (e) return e;
     } else {
       if ((e = rq_update<FT>(M, ld, 0, above, cb, L0, nbo, Vb, L0, Tb, ldt, S.ws[0], S.st))) return e;
     }
@@ -820,7 +892,8 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   const int L = std::max(R, C);
   const size_t wn = size_t(NB) * std::max(R, C) * 64;  // split-K partials (st)
   const size_t wn2 = size_t(NBO) * NBO * 64;            // split-K partials (s2)
-  const bool lows = sizeof(CT) == sizeof(FT);
+  const bool lows = P.u_s == 0;  // correction at u_s = low: one demotion scale (refine.hpp:103-119)
+  const bool lowf = P.u_f == 0;  // pre-scaling only at u_f = low (lse.hpp:315-318, gls.hpp:287-289)
 
   Arena ar;
   const size_t bytes = sizeof(FT) * (size_t(R) * C + size_t(obz) * R * NBO + size_t(obq) * C * NBO +
@@ -910,8 +983,8 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
     memcpy(&v, &b, 8);
     return v == 0.0 ? 1.0 : v;
   };
-  const double sA = asd(hb[0]), c1 = asd(hb[2]);
-  double sB = asd(hb[1]);
+  const double sA = lowf ? asd(hb[0]) : 1.0, c1 = lowf ? asd(hb[2]) : 1.0;
+  double sB = lowf ? asd(hb[1]) : 1.0;
   if (P.gmres) {
     // gmres_refine_lse (krylov.hpp:562-566): s_B = s_A ||B||_F / ||A||_F balances the blocks
     k_cast<FT, WT><<<grid, KT, 0, st>>>(gA, P.lda, rows1, cols1, 1.0, M, ld, parts);
@@ -1391,9 +1464,12 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
 }
 
 int large_solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
-  // u_f = working needs binary64 WY GEMMs and panels (not built yet); the
-  // extended residual is real-only (the reference has no complex path)
-  if (P.u_f != 0 || (P.u_r == 2 && P.cplx)) return MLSB_ERR_UNSUPPORTED;
+  // the extended residual is real-only (the reference has no complex path)
+  if (P.u_r == 2 && P.cplx) return MLSB_ERR_UNSUPPORTED;
+  if (P.u_f != 0) {  // binary64 factors: FP64 panels and WY GEMMs (real; the reference has no complex path)
+    if (P.cplx || P.gmres) return MLSB_ERR_UNSUPPORTED;
+    return solve<double, double, double>(P, st, out);
+  }
   if (P.cplx) {
     if (P.u_s != 0) return solve<cf, cd, cd>(P, st, out);
     return solve<cf, cd, cf>(P, st, out);

@@ -151,19 +151,17 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, T alpha,
 // allow it (VEC), staged in registers while the previous tile is consumed,
 // and transposed into the k-major shared layout on the store.
 template <bool HA, bool HB, bool VEC>
-__global__ void __launch_bounds__(256, 2) sgemm128(int M, int N, int K, float alpha,
-                                                   const float* __restrict__ A, int64_t lda,
-                                                   const float* __restrict__ B, int64_t ldb, float beta,
-                                                   float* __restrict__ C, int64_t ldc, int kchunk,
-                                                   int64_t split_stride) {
-  constexpr int BM = 128, BN = 128, BK = 16, LDS = BM + 4;
-  __shared__ __align__(16) float As[2][BK][LDS];
-  __shared__ __align__(16) float Bs[2][BK][LDS];
+__device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, const float* __restrict__ A,
+                                              int64_t lda, const float* __restrict__ B, int64_t ldb,
+                                              float beta, float* __restrict__ C, int64_t ldc, int kchunk,
+                                              int64_t split_stride, int bx, int by, int bz,
+                                              float (&As)[2][16][132], float (&Bs)[2][16][132]) {
+  constexpr int BM = 128, BN = 128, BK = 16;
   const int tid = threadIdx.x, tr = tid & 15, tc = tid >> 4;
-  const int i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
-  const int kbeg = blockIdx.z * kchunk;
+  const int i0 = bx * BM, j0 = by * BN;
+  const int kbeg = bz * kchunk;
   const int kend = min(K, kbeg + kchunk);
-  C += int64_t(blockIdx.z) * split_stride;
+  C += int64_t(bz) * split_stride;
 
   // staging: 512 float4 slots per operand tile, two per thread
   float ra[8], rb[8];
@@ -335,6 +333,26 @@ __global__ void __launch_bounds__(256, 2) sgemm128(int M, int N, int K, float al
   }
 }
 
+// Persistent form: the grid may be smaller than the tile count (gm x gn x gz),
+// each CTA walking tiles with a stride, so a trailing update can leave SMs
+// free for the look-ahead stream's panel cluster and small GEMMs.
+template <bool HA, bool HB, bool VEC>
+__global__ void __launch_bounds__(256, 2) sgemm128(int M, int N, int K, float alpha,
+                                                   const float* __restrict__ A, int64_t lda,
+                                                   const float* __restrict__ B, int64_t ldb, float beta,
+                                                   float* __restrict__ C, int64_t ldc, int kchunk,
+                                                   int64_t split_stride, int gm, int gn, int gz) {
+  __shared__ __align__(16) float As[2][16][132];
+  __shared__ __align__(16) float Bs[2][16][132];
+  const int ntiles = gm * gn * gz;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int bx = t % gm, by = (t / gm) % gn, bz = t / (gm * gn);
+    sgemm128_tile<HA, HB, VEC>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, split_stride, bx, by, bz,
+                               As, Bs);
+    __syncthreads();
+  }
+}
+
 // C[i + j ldc] = sum_z part[z][i + j M] + beta * C   (fixed split order)
 template <class T>
 __global__ void splitk_reduce(int M, int N, int splits, const T* __restrict__ part, int64_t stride,
@@ -370,6 +388,11 @@ template <> struct Tiles<float> {
   using Sq = Tile<128, 128, 8, 8>;
   using Tall = Tile<256, 32, 8, 4>;
   using Wide = Tile<32, 256, 4, 8>;
+};
+template <> struct Tiles<double> {  // binary64 (u_f = working): FP64 FMA, 4x4 per thread
+  using Sq = Tile<64, 64, 4, 4>;
+  using Tall = Tile<128, 32, 4, 4>;
+  using Wide = Tile<32, 128, 4, 4>;
 };
 template <> struct Tiles<cf> {
   using Sq = Tile<64, 64, 4, 4>;
@@ -407,18 +430,29 @@ static cudaError_t gemm_tile(bool ha, bool hb, int M, int N, int K, T alpha, con
   return cudaGetLastError();
 }
 
+// cap on resident CTAs of the big trailing GEMMs (0 = no cap), see sgemm128
+static thread_local int g_gemm_cta_cap = 0;
+void set_gemm_cta_cap(int cap) { g_gemm_cta_cap = cap; }
+
 template <bool VEC>
-static void launch128(bool ha, bool hb, dim3 grid, int M, int N, int K, float alpha, const float* A,
+static void launch128(bool ha, bool hb, dim3 tiles, int M, int N, int K, float alpha, const float* A,
                       int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc,
                       int kchunk, int64_t sstr, cudaStream_t st) {
+  const int nt = int(tiles.x * tiles.y * tiles.z);
+  const int grid = g_gemm_cta_cap > 0 ? std::min(nt, g_gemm_cta_cap) : nt;
+  const int gm = int(tiles.x), gn = int(tiles.y), gz = int(tiles.z);
   if (!ha && !hb)
-    sgemm128<false, false, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+    sgemm128<false, false, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr,
+                                                   gm, gn, gz);
   else if (ha && !hb)
-    sgemm128<true, false, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+    sgemm128<true, false, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr,
+                                                   gm, gn, gz);
   else if (!ha && hb)
-    sgemm128<false, true, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+    sgemm128<false, true, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr,
+                                                   gm, gn, gz);
   else
-    sgemm128<true, true, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+    sgemm128<true, true, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr,
+                                                   gm, gn, gz);
 }
 
 static cudaError_t sgemm_sq(bool ha, bool hb, int M, int N, int K, float alpha, const float* A, int64_t lda,
@@ -489,17 +523,39 @@ __global__ void __launch_bounds__(256) k_tmerge(int nbo, const T* __restrict__ G
   T* X = S + NBO * LDS;              // X[r + c NBO]
   const int tid = threadIdx.x;
   const int nblk = (nbo + NB - 1) / NB;
-  for (int e = tid; e < nbo * nbo; e += 256) {
-    const int r = e % nbo, c = e / nbo, br = r / NB, bc = c / NB;
-    S[r + c * LDS] = br == bc ? Tp[br * NB * NB + (r - br * NB) + (c - bc * NB) * NB] : zero<T>();
+  // diagonal blocks: loads issued in batches of 16 from clamped addresses
+  for (int e0 = tid; e0 < nbo * nbo; e0 += 256 * 16) {
+    T v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = min(e0 + 256 * u, nbo * nbo - 1), r = e % nbo, c = e / nbo, br = r / NB;
+      v[u] = Tp[br * NB * NB + (r - br * NB) + (c % NB) * NB];
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = e0 + 256 * u;
+      if (e < nbo * nbo) {
+        const int r = e % nbo, c = e / nbo;
+        S[r + c * LDS] = (r / NB == c / NB) ? v[u] : zero<T>();
+      }
+    }
   }
   __syncthreads();
   T* GX = X + NBO * NB;  // staged block column G[0:h, c0:c0+w]
   for (int j = 1; j < nblk; ++j) {
     const int c0 = j * NB, w = min(NB, nbo - c0), h = c0;
-    for (int e = tid; e < h * w; e += 256) {
-      const int r = e % h, c = e / h;
-      GX[r + c * NBO] = G[r + int64_t(c0 + c) * ldg];
+    for (int e0 = tid; e0 < h * w; e0 += 256 * 12) {
+      T v[12];
+#pragma unroll
+      for (int u = 0; u < 12; ++u) {
+        const int e = min(e0 + 256 * u, h * w - 1);
+        v[u] = G[e % h + int64_t(c0 + e / h) * ldg];
+      }
+#pragma unroll
+      for (int u = 0; u < 12; ++u) {
+        const int e = e0 + 256 * u;
+        if (e < h * w) GX[e % h + (e / h) * NBO] = v[u];
+      }
     }
     __syncthreads();
     for (int e = tid; e < h * w; e += 256) {
@@ -544,11 +600,20 @@ cudaError_t tmerge_f32(int nbo, const float* G, int ldg, const float* Tp, float*
 cudaError_t tmerge_c64(int nbo, const cf* G, int ldg, const cf* Tp, cf* Tout, int ldt, cudaStream_t st) {
   return tmerge_t<cf>(nbo, G, ldg, Tp, Tout, ldt, st);
 }
+cudaError_t tmerge_f64(int nbo, const double* G, int ldg, const double* Tp, double* Tout, int ldt,
+                       cudaStream_t st) {
+  return tmerge_t<double>(nbo, G, ldg, Tp, Tout, ldt, st);
+}
 
 cudaError_t gemm_f32(bool ha, bool hb, int M, int N, int K, float alpha, const float* A,
                      int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc,
                      float* work, size_t work_elems, cudaStream_t st) {
   return gemm_t<float>(ha, hb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, work, work_elems, st);
+}
+cudaError_t gemm_f64(bool ha, bool hb, int M, int N, int K, double alpha, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double beta, double* C, int64_t ldc, double* work,
+                     size_t work_elems, cudaStream_t st) {
+  return gemm_t<double>(ha, hb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, work, work_elems, st);
 }
 cudaError_t gemm_c64(bool ha, bool hb, int M, int N, int K, cf alpha, const cf* A, int64_t lda,
                      const cf* B, int64_t ldb, cf beta, cf* C, int64_t ldc, cf* work,

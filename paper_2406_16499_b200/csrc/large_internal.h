@@ -15,9 +15,16 @@ namespace lg {
 cudaError_t gemm_f32(bool ha, bool hb, int M, int N, int K, float alpha, const float* A,
                      int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc,
                      float* work, size_t work_elems, cudaStream_t st);
+cudaError_t gemm_f64(bool ha, bool hb, int M, int N, int K, double alpha, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double beta, double* C, int64_t ldc, double* work,
+                     size_t work_elems, cudaStream_t st);
 cudaError_t gemm_c64(bool ha, bool hb, int M, int N, int K, cf alpha, const cf* A, int64_t lda,
                      const cf* B, int64_t ldb, cf beta, cf* C, int64_t ldc, cf* work,
                      size_t work_elems, cudaStream_t st);
+
+// cap on the resident CTAs of the binary32 WY GEMMs issued by this host thread
+// (0 = none): the trailing updates leave SMs to the look-ahead stream
+void set_gemm_cta_cap(int cap);
 
 constexpr int NB = 32;       // reflectors per panel / WY block
 constexpr int NBO = 128;     // reflectors per outer block (one trailing update)
@@ -28,6 +35,8 @@ constexpr int PCL = 16;      // CTAs per panel cluster
 cudaError_t tmerge_f32(int nbo, const float* G, int ldg, const float* Tp, float* Tout, int ldt,
                        cudaStream_t st);
 cudaError_t tmerge_c64(int nbo, const cf* G, int ldg, const cf* Tp, cf* Tout, int ldt, cudaStream_t st);
+cudaError_t tmerge_f64(int nbo, const double* G, int ldg, const double* Tp, double* Tout, int ldt,
+                       cudaStream_t st);
 
 // One panel of NB Householder reflectors, factored by a PCL-CTA cluster.
 // QR view P (L x nb): P[r][q] = M[r0 + r, c0 + q]           (rq = false)

@@ -74,6 +74,18 @@ __device__ __forceinline__ void larfg_s(float alpha, double ss, float& tau, floa
     beta = bt;
   }
 }
+// binary64 factors (u_f = working): the reference's make_reflector in double
+__device__ __forceinline__ void larfg_s(double alpha, double ss, double& tau, double& inv, double& beta) {
+  tau = 0.0;
+  inv = 1.0;
+  beta = alpha;
+  if (ss != 0.0) {
+    const double bt = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+    tau = (bt - alpha) / bt;
+    inv = 1.0 / (alpha - bt);
+    beta = bt;
+  }
+}
 __device__ __forceinline__ void larfg_s(cf alpha, double ss, cf& tau, cf& inv, cf& beta) {
   tau = cf{0.f, 0.f};
   inv = cf{1.f, 0.f};
@@ -603,12 +615,12 @@ cudaError_t panel_factor(T* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb
   }
   const size_t sm = panel_smem<T>(a.rc);
   auto kern = panel_kernel<T>;
-  static bool attr_done[2] = {false, false};
-  if (!attr_done[sizeof(T) == 8]) {
+  static bool attr_done = false;  // per instantiation
+  if (!attr_done) {
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1))) return e;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
       return e;
-    attr_done[sizeof(T) == 8] = true;
+    attr_done = true;
   }
   if (sm > 227 * 1024) return cudaErrorInvalidValue;
   cfg.gridDim = dim3(a.ncl);
@@ -621,6 +633,8 @@ template cudaError_t panel_factor<float>(float*, int64_t, int64_t, int64_t, int,
                                          float*, int64_t, float*, int64_t, cudaStream_t, long long*);
 template cudaError_t panel_factor<cf>(cf*, int64_t, int64_t, int64_t, int, int, bool, cf*, cf*,
                                       int64_t, cf*, int64_t, cudaStream_t, long long*);
+template cudaError_t panel_factor<double>(double*, int64_t, int64_t, int64_t, int, int, bool, double*,
+                                          double*, int64_t, double*, int64_t, cudaStream_t, long long*);
 
 }  // namespace lg
 }  // namespace mlsb

@@ -195,3 +195,45 @@ def test_lse_large_size_extended(gpu, port):
     assert res.trace.status == ref.status == "converged"
     assert abs(res.trace.iterations - ref.iterations) <= 1
     assert rel(res.state.x, ref.x) <= fwd_bound(1024, 512, 128, 1e5 * 10)
+
+
+# u_f = working on the large path: binary64 panels and WY GEMMs, no pre-scaling
+# (lse.hpp:315-318), correction without demotion (lse.hpp:399-411)
+@pytest.mark.parametrize("shape", [(20, 10, 4), (70, 40, 33), (300, 170, 40)])
+def test_lse_large_path_working_factor(gpu, port, force_large, shape):
+    m, n, p = shape
+    A, B, b, d = G.lse_problem(m, n, p, 1e6, 1e2, seed=m + 3 * n + p)
+    cfg = gpu.RefinementConfig(maxit=10, precisions=gpu.PrecisionConfig("working", "working"))
+    res = gpu.mplse(gpu.LseProblem(A, B, b, d), cfg)
+    ref = port.mplse(A, B, b, d, maxit=10, prec=("d", "d", "d"))
+    kappa = np.linalg.cond(np.vstack([A, B])) * 1e2
+    msgs = check_parity("lse", rel(res.state.x, ref.x), fwd_bound(m, n, p, kappa), res.trace.iterations,
+                        ref.iterations, lse_backward(A, B, b, d, res.state.x, res.state.r, res.state.v),
+                        lse_backward(A, B, b, d, ref.x, ref.r, ref.v), res.trace.status, ref.status)
+    assert res.trace.status == ref.status
+    assert not msgs, msgs
+
+
+@pytest.mark.parametrize("shape", [(40, 20, 30), (260, 120, 200)])
+def test_gls_large_path_working_factor(gpu, port, force_large, shape):
+    n, m, p = shape
+    W, V, d = G.gls_problem(n, m, p, 1e6, 1e2, seed=n + 3 * m + p)
+    cfg = gpu.RefinementConfig(maxit=10, precisions=gpu.PrecisionConfig("working", "working"))
+    res = gpu.mpgls(gpu.GlsProblem(W, V, d), cfg)
+    ref = port.mpgls(W, V, d, maxit=10, prec=("d", "d", "d"))
+    kappa = np.linalg.cond(np.hstack([W, V])) * 1e2
+    fwd = max(rel(res.state.x, ref.x), rel(res.state.y, ref.r))
+    msgs = check_parity("gls", fwd, fwd_bound(m, n, p, kappa), res.trace.iterations, ref.iterations,
+                        gls_backward(W, V, d, res.state.x, res.state.y, res.state.z),
+                        gls_backward(W, V, d, ref.x, ref.r, ref.v), res.trace.status, ref.status)
+    assert res.trace.status == ref.status
+    assert not msgs, msgs
+
+
+def test_lse_direct_large(gpu, port):
+    """binary64 direct solve (lse_direct, lse.hpp:132-152) at a size beyond the tile solver."""
+    A, B, b, d = G.lse_problem(1024, 512, 128, 1e4, 1e2, seed=21)
+    st = gpu.lse_direct(gpu.LseProblem(A, B, b, d))
+    xr, rr, vr = port.lse_direct(A, B, b, d)
+    assert rel(st.x, xr) <= fwd_bound(1024, 512, 128, 1e4 * 10)
+    assert rel(st.r, rr) <= fwd_bound(1024, 512, 128, 1e4 * 10)

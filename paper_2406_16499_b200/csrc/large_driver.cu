@@ -79,14 +79,33 @@ template <class T>
 __global__ void k_neg(T* x, int n) {
   for (int i = blockIdx.x * KT + threadIdx.x; i < n; i += gridDim.x * KT) x[i] = -x[i];
 }
-// r_f = b_f - A_f x_f, A_f = fl(A * inv) in the factor precision (lse.hpp:353-355)
+// r_f = b_f - A_f x_f, A_f = fl(A * inv) in the factor precision (lse.hpp:353-355):
+// column tiles of GNC (thread per row, loads in batches of 16 from a running
+// pointer) write partials that k_rowgemv_red sums in tile order
 template <class FT, class WT>
-__global__ void k_rowgemv_cast(const WT* A, int64_t lda, int rows, int cols, double inv,
-                               const FT* x, const FT* bf, FT* rf) {
+__global__ void __launch_bounds__(KT) k_rowgemv_cast(const WT* A, int64_t lda, int rows, int cols, double inv,
+                                                     const FT* x, FT* part) {
+  const int i = blockIdx.x * KT + threadIdx.x, j0 = blockIdx.y * GNC, jn = min(GNC, cols - j0);
+  if (i >= rows) return;
+  FT acc = zero<FT>();
+  const WT* p = A + i + int64_t(j0) * lda;
+  for (int jb = 0; jb < jn; jb += 16) {
+    WT t[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) t[u] = jb + u < jn ? p[int64_t(u) * lda] : zero<WT>();
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (jb + u < jn) mac(acc, narrow<FT>(scale<WT>(inv, t[u])), x[j0 + jb + u]);
+    p += int64_t(16) * lda;
+  }
+  part[int64_t(blockIdx.y) * rows + i] = acc;
+}
+template <class FT>
+__global__ void k_rowgemv_red(const FT* part, int rows, int ntiles, const FT* bf, FT* rf) {
   for (int i = blockIdx.x * KT + threadIdx.x; i < rows; i += gridDim.x * KT) {
-    FT acc = zero<FT>();
-    for (int j = 0; j < cols; ++j) mac(acc, narrow<FT>(scale<WT>(inv, A[i + int64_t(j) * lda])), x[j]);
-    rf[i] = bf[i] - acc;
+    FT s = zero<FT>();
+    for (int t = 0; t < ntiles; ++t) s = s + part[int64_t(t) * rows + i];
+    rf[i] = bf[i] - s;
   }
 }
 // max |x| over n entries (bits, NaN skipped)
@@ -1112,7 +1131,12 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
     k_copy<FT><<<nblk(p), KT, 0, st>>>(y2, p, y + k);
     trsv<FT, FT>(M, ld, 0, 0, k, false, y, st);             // T11 y1 = c1 - T12 y2
     apply_F<FT, FT>(FQ, false, y, ypf, st);                  // x = Q^H [y1; y2]  (F_Q = Q^H)
-    k_rowgemv_cast<FT, WT><<<nblk(m), KT, 0, st>>>(gA, P.lda, m, n, 1.0 / sA, y, bf, rf);
+    {
+      const int nt = (n + GNC - 1) / GNC;  // gscr_f / gscr hold L * ceil(L / GNC) entries
+      FT* part = std::is_same<FT, CT>::value ? reinterpret_cast<FT*>(gscr) : gscr_f;
+      k_rowgemv_cast<FT, WT><<<dim3((m + KT - 1) / KT, nt), KT, 0, st>>>(gA, P.lda, m, n, 1.0 / sA, y, part);
+      k_rowgemv_red<FT><<<nblk(m), KT, 0, st>>>(part, m, nt, bf, rf);
+    }
     k_convert<FT, WT><<<nblk(n), KT, 0, st>>>(y, n, su);
     k_convert<FT, WT><<<nblk(m), KT, 0, st>>>(rf, m, sw);
     // solve_v (lse.hpp:156-165): g = A^H r at u_r, sigma, Q g, R^H v = g(n-p:n)

@@ -139,6 +139,18 @@ int mlsb_gmres_lse(const double* A, int64_t lda, const double* B, int64_t ldb, c
                    int precond, double alpha_scale, double* x, double* r, double* v,
                    mlsb_trace* trace, int64_t* singular_index, const mlsb_exec* exec);
 
+/* GMRES-IR for GLS (gmres_refine_gls, inc/krylov.hpp:673-784): the outer
+ * loop of mpgls with each correction solved by full MGS-GMRES on the alpha-
+ * scaled GLS augmented operator [a I_p V^T 0; V 0 W; 0 W^T 0] (krylov.hpp:
+ * 24-26), alpha = alpha_scale * ||y0||, pre-scaling s_W = s_V ||W||_F/||V||_F.
+ * precond: MLSB_PRECOND_LEFT (left_gls_apply, krylov.hpp:232-250, cascade
+ * initial guess) or MLSB_PRECOND_BD_SPLIT (bd_gls_apply, krylov.hpp:288-321,
+ * both the n <= p and the n > p case).  Built for u_f = low. */
+int mlsb_gmres_gls(const double* W, int64_t ldw, const double* V, int64_t ldv, const double* d,
+                   int64_t n, int64_t m, int64_t p, const mlsb_config* cfg, int precond,
+                   double alpha_scale, double* x, double* y, double* z, mlsb_trace* trace,
+                   int64_t* singular_index, const mlsb_exec* exec);
+
 /* Complex128 problems (interleaved re, im; same shapes and semantics with
  * Hermitian transposes), solved with complex64 factors at u_f = low.  The
  * reference is real-only; these serve BASELINE config 5. */

@@ -243,6 +243,31 @@ class Oracle:
         return OracleResult(x, r, v, STATUS[st.value], it.value,
                             hist[: 3 * it.value].reshape(-1, 3), inner=inner.value)
 
+    def gmres_gls(self, W, V, d, tol=1e-13, maxit=40, prec=("s", "s", "d"), precond="bd_split",
+                  alpha_scale=1.0):
+        """gmres_refine_gls (krylov.hpp:673) -- reference build only.  Returns
+        (x, y, z) as OracleResult(x, r=y, v=z)."""
+        if not hasattr(self.lib, "orc_gmres_gls"):
+            raise OracleError(9)
+        n, m = W.shape
+        p = V.shape[1]
+        W, V = _f(W), _f(V)
+        d = np.ascontiguousarray(d, np.float64)
+        x, y, z = np.zeros(m), np.zeros(p), np.zeros(n)
+        st, it, inner = C.c_int32(0), C.c_int64(0), C.c_int64(0)
+        hist = np.zeros(3 * max(maxit, 1))
+        sing = C.c_int64(-1)
+        uf, us, ur = (LEVEL[q] for q in prec)
+        f = self.lib.orc_gmres_gls
+        f.restype = C.c_int
+        rc = f(_i64(n), _i64(m), _i64(p), _p(W), _p(V), _p(d), C.c_double(tol), _i64(maxit), C.c_int(uf),
+               C.c_int(us), C.c_int(ur), C.c_int(0 if precond == "left" else 1), C.c_double(alpha_scale),
+               _p(x), _p(y), _p(z), C.byref(st), C.byref(it), C.byref(inner), _p(hist), C.byref(sing))
+        if rc:
+            raise OracleError(rc, sing.value)
+        return OracleResult(x, y, z, STATUS[st.value], it.value,
+                            hist[: 3 * it.value].reshape(-1, 3), inner=inner.value)
+
     def lse_direct(self, A, B, b, d):
         m, n = A.shape
         p = B.shape[0]

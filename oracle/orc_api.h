@@ -73,6 +73,12 @@ int orc_gmres_lse(int64_t m, int64_t n, int64_t p, const double* A, const double
                   int ur, int precond, double alpha_scale, double* x, double* r, double* v,
                   int32_t* status, int64_t* iters, int64_t* inner, double* hist, int64_t* sing);
 
+/* GMRES-IR for GLS (inc/krylov.hpp:673 gmres_refine_gls), reference build only */
+int orc_gmres_gls(int64_t n, int64_t m, int64_t p, const double* W, const double* V,
+                  const double* d, double tol, int64_t maxit, int uf, int us, int ur, int precond,
+                  double alpha_scale, double* x, double* y, double* z, int32_t* status,
+                  int64_t* iters, int64_t* inner, double* hist, int64_t* sing);
+
 /* binary64 direct solves (the err-2 / er-2 denominators, inc/experiment.hpp:50-73) */
 int orc_lse_direct(int64_t m, int64_t n, int64_t p, const double* A, const double* B,
                    const double* b, const double* d, double* x, double* r, double* v,

@@ -11,7 +11,7 @@
 //   lse_correction_solve inc/lse.hpp:84, gls_correction_solve inc/gls.hpp:107
 //   lse_direct inc/lse.hpp:132, gls_direct inc/gls.hpp:85
 //   gen_lse_problem / gen_gls_problem inc/generate.hpp:60-106
-//   gmres_refine_lse inc/krylov.hpp:545
+//   gmres_refine_lse inc/krylov.hpp:545, gmres_refine_gls inc/krylov.hpp:673
 #include <algorithm>
 #include <atomic>
 #include <cstring>
@@ -145,6 +145,25 @@ int orc_gmres_lse(int64_t m, int64_t n, int64_t p, const double* A, const double
             put(res.state.x, x);
             put(res.state.r, r);
             put(res.state.v, v);
+            put_trace(res.trace, status, iters, hist, nullptr);
+            if (inner) *inner = static_cast<int64_t>(res.trace.inner_iterations);
+        },
+        sing);
+}
+
+int orc_gmres_gls(int64_t n, int64_t m, int64_t p, const double* W, const double* V,
+                  const double* d, double tol, int64_t maxit, int uf, int us, int ur, int precond,
+                  double alpha_scale, double* x, double* y, double* z, int32_t* status,
+                  int64_t* iters, int64_t* inner, double* hist, int64_t* sing) {
+    return guarded(
+        [&] {
+            auto pb = make_gls(n, m, p, W, V, d);
+            auto res = gmres_refine_gls(pb, make_cfg(tol, maxit, uf, us, ur),
+                                        precond == 0 ? precond_choice::left : precond_choice::bd_split,
+                                        alpha_scale);
+            put(res.state.x, x);
+            put(res.state.y, y);
+            put(res.state.z, z);
             put_trace(res.trace, status, iters, hist, nullptr);
             if (inner) *inner = static_cast<int64_t>(res.trace.inner_iterations);
         },

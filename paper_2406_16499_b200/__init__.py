@@ -46,6 +46,7 @@ from .api import (  # noqa: F401
     RefinementTrace,
     gls_direct,
     gmres_refine_lse,
+    gmres_refine_gls,
     lse_direct,
     mpgls,
     mpgls_batched,
@@ -56,6 +57,6 @@ from .api import (  # noqa: F401
 __all__ = [
     "LseProblem", "GlsProblem", "LseState", "GlsState", "PrecisionConfig", "RefinementConfig",
     "RefinementTrace", "MplseResult", "MpglsResult", "mplse", "mpgls", "mplse_batched",
-    "mpgls_batched", "lse_direct", "gls_direct", "gmres_refine_lse", "MixedlsError", "DimensionError", "InvalidInput", "SingularTriangular",
+    "mpgls_batched", "lse_direct", "gls_direct", "gmres_refine_lse", "gmres_refine_gls", "MixedlsError", "DimensionError", "InvalidInput", "SingularTriangular",
     "CudaError", "Unsupported", "lib", "lib_path",
 ]

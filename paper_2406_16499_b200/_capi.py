@@ -79,11 +79,13 @@ def _load():
                                      dp, dp, dp, i32p, dp, i32p, dp, dp, exp_]
     L.mlsb_gmres_lse.argtypes = [dp, i64, dp, i64, dp, dp, i64, i64, i64, cfgp, C.c_int, C.c_double,
                                  dp, dp, dp, trp, i64p, exp_]
+    L.mlsb_gmres_gls.argtypes = [dp, i64, dp, i64, dp, i64, i64, i64, cfgp, C.c_int, C.c_double,
+                                 dp, dp, dp, trp, i64p, exp_]
     L.mlsb_lse_direct.argtypes = [dp, i64, dp, i64, dp, dp, i64, i64, i64, dp, dp, dp, i64p, exp_]
     L.mlsb_gls_direct.argtypes = [dp, i64, dp, i64, dp, i64, i64, i64, dp, dp, dp, i64p, exp_]
     for f in ("mlsb_mplse", "mlsb_mpgls", "mlsb_mplse_batched", "mlsb_mpgls_batched",
               "mlsb_mplse_z", "mlsb_mpgls_z", "mlsb_lse_direct", "mlsb_gls_direct",
-              "mlsb_gmres_lse"):
+              "mlsb_gmres_lse", "mlsb_gmres_gls"):
         getattr(L, f).restype = C.c_int
     return L
 

@@ -275,6 +275,49 @@ def gmres_refine_lse(pb: LseProblem, cfg: RefinementConfig | None = None,
     return MplseResult(LseState(x, r, v), _trace_from(tr, hist))
 
 
+def gmres_refine_gls(pb: GlsProblem, cfg: RefinementConfig | None = None,
+                     precond: str = "bd_split", alpha_scale: float = 1.0,
+                     stream=None) -> MpglsResult:
+    """GMRES-IR for GLS (gmres_refine_gls, inc/krylov.hpp:673-784) on the GPU:
+    precond "left" or "bd_split"; trace.inner_iterations = total GMRES steps."""
+    cfg = cfg or RefinementConfig()
+    ccfg = cfg.to_c()
+    if precond not in ("left", "bd_split"):
+        raise _capi.InvalidInput("gmres: precond must be 'left' or 'bd_split'")
+    dev = _is_cuda(pb.W)
+    if dev:
+        import torch
+
+        W, V, d = pb.W, pb.V, pb.d
+        n, m, ldw = _matrix_ld(W)
+        _, p, ldv = _matrix_ld(V)
+        x = torch.empty(m, dtype=torch.float64, device=W.device)
+        y = torch.empty(p, dtype=torch.float64, device=W.device)
+        z = torch.empty(n, dtype=torch.float64, device=W.device)
+    else:
+        W = np.asfortranarray(pb.W, dtype=np.float64)
+        V = np.asfortranarray(pb.V, dtype=np.float64)
+        if W.ndim != 2 or V.ndim != 2 or V.shape[0] != W.shape[0]:
+            raise _capi.DimensionError("gls_problem: W and V row counts differ")
+        d = np.ascontiguousarray(pb.d, dtype=np.float64)
+        n, m = W.shape
+        p = V.shape[1]
+        if d.shape != (n,):
+            raise _capi.DimensionError("gls_problem: rhs length mismatch")
+        ldw = ldv = max(n, 1)
+        x, y, z = np.zeros(m), np.zeros(p), np.zeros(n)
+    hist = np.zeros(3 * max(int(cfg.maxit), 1))
+    tr = Trace()
+    tr.residual_history = hist.ctypes.data_as(C.POINTER(C.c_double))
+    sing = C.c_int64(-1)
+    ex = _exec(dev, stream)
+    rc = lib.mlsb_gmres_gls(_ptr(W), ldw, _ptr(V), ldv, _ptr(d), n, m, p, C.byref(ccfg),
+                            0 if precond == "left" else 1, float(alpha_scale), _ptr(x), _ptr(y),
+                            _ptr(z), C.byref(tr), C.byref(sing), C.byref(ex))
+    raise_for(rc, sing.value)
+    return MpglsResult(GlsState(x, y, z), _trace_from(tr, hist))
+
+
 def lse_direct(pb: LseProblem, stream=None) -> LseState:
     """binary64 direct LSE solve on the GPU: the err-2 reference of the experiment
     harness (detail::lse_direct_reference, inc/experiment.hpp:50-59)."""

@@ -720,6 +720,28 @@ int mlsb_gmres_lse(const double* A, int64_t lda, const double* B, int64_t ldb, c
                      precond == MLSB_PRECOND_LEFT ? 1 : 2, alpha_scale);
 }
 
+int mlsb_gmres_gls(const double* W, int64_t ldw, const double* V, int64_t ldv, const double* d,
+                   int64_t n, int64_t m, int64_t p, const mlsb_config* cfg, int precond,
+                   double alpha_scale, double* x, double* y, double* z, mlsb_trace* trace,
+                   int64_t* singular_index, const mlsb_exec* exec) {
+  // gmres_refine_gls (krylov.hpp:673): same validation as mpgls
+  if (n <= 0 || m <= 0 || p <= 0) return fail(MLSB_ERR_DIMENSION, "gls_problem: empty matrix");
+  if (m > n || n > m + p) return fail(MLSB_ERR_DIMENSION, "gls_problem: requires m <= n <= m + p");
+  if (ldw < n || ldv < n) return fail(MLSB_ERR_DIMENSION, "gls_problem: leading dimension too small");
+  if (!W || !V || !d) return fail(MLSB_ERR_DIMENSION, "gls_problem: null input");
+  if (int rc = check_config(cfg)) return rc;
+  if (precond != MLSB_PRECOND_LEFT && precond != MLSB_PRECOND_BD_SPLIT)
+    return fail(MLSB_ERR_INVALID_INPUT, "gmres: unknown preconditioner");
+  if (!(alpha_scale > 0.0)) return fail(MLSB_ERR_INVALID_INPUT, "gmres: alpha_scale must be positive");
+  if (cfg->u_f != MLSB_LOW) return fail(MLSB_ERR_UNSUPPORTED, "gmres: built for u_f = low");
+  if (int rc = check_device()) return rc;
+  DevScope scope(exec);
+  if (!scope.ok) return fail(MLSB_ERR_CUDA, "cudaSetDevice failed");
+  return solve_large(gls_shape(n, m, p), 8, W, ldw, V, ldv, nullptr, d, cfg, x, y, z, trace,
+                     singular_index, exec, false, nullptr, nullptr, nullptr, nullptr,
+                     precond == MLSB_PRECOND_LEFT ? 1 : 2, alpha_scale);
+}
+
 int mlsb_mplse_z(const double* A, int64_t lda, const double* B, int64_t ldb, const double* b,
                  const double* d, int64_t m, int64_t n, int64_t p, const mlsb_config* cfg,
                  double* x, double* r, double* v, mlsb_trace* trace, int64_t* singular_index,

@@ -752,39 +752,179 @@ static void gm_cascade(int m, int n, int p, const FT* M, int64_t ld, const Fac<F
   k_copy<double><<<nblk(p), KT, 0, st>>>(t4, p, dv);
 }
 
-// One GMRES-IR correction (krylov.hpp:640-681): rhs from the residual blocks,
-// optional cascade initial guess (left), full MGS-GMRES with Givens rotations
-// (krylov.hpp:436-512, rel_tol 1e-6, max_iter N) and the state update.
+// ---------------------------------------------------------- GMRES-IR (GLS)
+// Augmented vectors are ordered [y-block (p); z-block (n); x-block (m)]
+// (krylov.hpp:24-26).  In the packed GLS factors M (n x (m+p)): R = M[0:m, 0:m],
+// T(i, j) = M[i, m + j]; F_Z (the driver's QR factor) is Q, F_Q (the RQ factor)
+// is Z^H: Q x = apply_F(FZ, false), Q^T x = apply_F(FZ, true), Z x =
+// apply_F(FQ, true), Z^T x = apply_F(FQ, false).
+
+// out = op(u) (augmented_operator::apply, GLS branch); tmp holds [u3; u1]
+static void gm_op_gls(int n, int m, int p, double alpha, const double* gW, const double* gV, int64_t ldw,
+                      int64_t ldv, double sW, double sV, const double* u, double* out, double* tmp,
+                      double* rpart, double* cpart, cudaStream_t st) {
+  const int R = n, C = m + p;
+  const int ntr = (R + RTR - 1) / RTR, ntc = (C + RTC - 1) / RTC;
+  k_copy<double><<<nblk(m), KT, 0, st>>>(u + p + n, m, tmp);
+  k_copy<double><<<nblk(p), KT, 0, st>>>(u, p, tmp + m);
+  const StackX SX{gW, gV, ldw, ldv, m, false, sW, sV};
+  dim3 g2(ntr, ntc);
+  k_resid_tile<double, StackX><<<g2, KT, 0, st>>>(SX, R, C, tmp, u + p, rpart, cpart);
+  k_op_reduce_gls<<<nblk(p + n + m), KT, 0, st>>>(n, m, p, ntc, ntr, rpart, cpart, u, alpha, out);
+}
+
+// block-diagonal split preconditioner for GLS (bd_gls_apply, krylov.hpp:288-321),
+// both cases: n <= p (T2 = T(0:n, p-n:p)) and n > p (U = [I T1; 0 T2],
+// Y = [I T1(:, 0:k); 0 T2(0:k, 0:k)], k = m - (n - p), applied blockwise)
 template <class FT>
-static int gmres_correction(int kind, int m, int n, int p, double alpha, const FT* M, int64_t ld,
-                            const Fac<FT>& FZ, const Fac<FT>& FQ, const double* gA, const double* gB,
-                            int64_t lda, int64_t ldb, double sA, double sB, const double* rout,
-                            const double* cout, double* sw, double* su, double* rhs, double* wacc,
-                            double* t1, double* t2, double* t3, double* t4, double* part, int nb,
-                            double* hdev, GmBuf& bas, int& cap, double* const* cv, double* ypart,
-                            double* rpart, double* cpart, int* flag, int64_t* its_out,
-                            cudaStream_t st) {
-  const int N = m + p + n;
-  const double sqa = sqrt(alpha);
-  cudaError_t e;
-  k_scal<<<nblk(m + p), KT, 0, st>>>(sqa, rout, m + p, rhs);
-  k_scal<<<nblk(n), KT, 0, st>>>(1.0 / sqa, cout, n, rhs + m + p);
-  k_fill<double><<<nblk(N), KT, 0, st>>>(wacc, N, 0.0);
-  if (kind == 1) {  // cascade initial guess: the left preconditioner is singular on null(B)
-    gm_cascade<FT>(m, n, p, M, ld, FZ, FQ, rout, rout + m, cout, cv, ypart, t1, t1 + m, t1 + m + p, st);
-    k_scal<<<nblk(m), KT, 0, st>>>(1.0 / sqa, t1, m, wacc);
-    k_scal<<<nblk(p), KT, 0, st>>>(-1.0 / sqa, t1 + m, p, wacc + m);
-    k_scal<<<nblk(n), KT, 0, st>>>(sqa, t1 + m + p, n, wacc + m + p);
-    gm_op(m, n, p, alpha, gA, gB, lda, ldb, sA, sB, wacc, t2, rpart, cpart, st);
-    k_axpy<<<nblk(N), KT, 0, st>>>(-1.0, t2, N, rhs);
+static void gm_bd_gls(bool left, int n, int m, int p, double alpha, const FT* M, int64_t ld,
+                      const Fac<FT>& FZ, const double* w, double* out, double* ta, double* tb,
+                      double* tc, double* ypart, cudaStream_t st) {
+  const double ra = 1.0 / sqrt(alpha), sa = sqrt(alpha);
+  const Mask none{0, 0, 0};
+  const int kk = std::min(n, p);
+  const Mask rqm{2, n - kk, m + (p - kk)};
+  double* o2 = out + p;
+  double* o3 = out + p + n;
+  k_copy<double><<<nblk(n), KT, 0, st>>>(w + p, n, ta);      // w2
+  k_copy<double><<<nblk(m), KT, 0, st>>>(w + p + n, m, tb);  // w3
+  if (n <= p) {
+    if (left) {
+      apply_F<FT, double>(FZ, true, ta, ypart, st);                  // q = Q^T w2
+      trsv<FT, double>(M, ld, 0, m + p - n, n, false, ta, st);       // T2 o2 = q
+      trsv<FT, double>(M, ld, 0, 0, m, true, tb, st);                // R^T t = w3
+      gemv_h<FT, double>(M, ld, 0, m, m + p - n, m, rqm, tb, o3, st);  // o3 = T(0:m, p-n:p-n+m)^T t
+      k_copy<double><<<nblk(n), KT, 0, st>>>(ta, n, o2);
+    } else {
+      trsv<FT, double>(M, ld, 0, m + p - n, n, true, ta, st);        // T2^T t = w2
+      apply_F<FT, double>(FZ, false, ta, ypart, st);                 // o2 = Q t
+      gemv_n<FT, double>(M, ld, 0, m, m + p - n, m, rqm, tb, o3, st);  // t3 = T(0:m, p-n:..) w3
+      trsv<FT, double>(M, ld, 0, 0, m, false, o3, st);               // o3 = R^-1 t3
+      k_copy<double><<<nblk(n), KT, 0, st>>>(ta, n, o2);
+    }
+  } else {
+    const int d = n - p, k = m - d;
+    if (left) {
+      // o2 = U^-1 (Q^T w2): bottom T2 o_b = q_b, top o_t = q_t - T1 o_b
+      apply_F<FT, double>(FZ, true, ta, ypart, st);
+      trsv<FT, double>(M, ld, d, m, p, false, ta + d, st);
+      gemv_n<FT, double>(M, ld, 0, d, m, p, none, ta + d, tc, st);
+      k_sub<double><<<nblk(d), KT, 0, st>>>(ta, tc, d, ta);
+      k_copy<double><<<nblk(n), KT, 0, st>>>(ta, n, o2);
+      // o3 = Y^T (R^-T w3): top v_t, bottom T1(:,0:k)^T v_t + T2(0:k,0:k)^T v_b
+      trsv<FT, double>(M, ld, 0, 0, m, true, tb, st);
+      gemv_h<FT, double>(M, ld, 0, d, m, k, none, tb, tc, st);
+      gemv_h<FT, double>(M, ld, d, k, m, k, rqm, tb + d, tc + k, st);
+      k_copy<double><<<nblk(d), KT, 0, st>>>(tb, d, o3);
+      k_fill<double><<<nblk(k), KT, 0, st>>>(o3 + d, k, 0.0);
+      k_axpy<<<nblk(k), KT, 0, st>>>(1.0, tc, k, o3 + d);
+      k_axpy<<<nblk(k), KT, 0, st>>>(1.0, tc + k, k, o3 + d);
+    } else {
+      // o2 = Q U^-T w2: top t_t = w2_t, bottom T2^T t_b = w2_b - T1^T t_t
+      gemv_h<FT, double>(M, ld, 0, d, m, p, none, ta, tc, st);
+      k_sub<double><<<nblk(p), KT, 0, st>>>(ta + d, tc, p, ta + d);
+      trsv<FT, double>(M, ld, d, m, p, true, ta + d, st);
+      apply_F<FT, double>(FZ, false, ta, ypart, st);
+      k_copy<double><<<nblk(n), KT, 0, st>>>(ta, n, o2);
+      // o3 = R^-1 (Y w3): top w3_t + T1(:,0:k) w3_b, bottom T2(0:k,0:k) w3_b
+      gemv_n<FT, double>(M, ld, 0, d, m, k, none, tb + d, tc, st);
+      gemv_n<FT, double>(M, ld, d, k, m, k, rqm, tb + d, o3 + d, st);
+      k_copy<double><<<nblk(d), KT, 0, st>>>(tb, d, o3);
+      k_axpy<<<nblk(d), KT, 0, st>>>(1.0, tc, d, o3);
+      trsv<FT, double>(M, ld, 0, 0, m, false, o3, st);
+    }
   }
-  auto lp = [&](const double* in, double* o) {
-    if (kind == 2) gm_bd<FT>(true, m, n, p, alpha, M, ld, FQ, in, o, cv[8], cv[9], ypart, st);
-    else gm_left<FT>(m, n, p, alpha, M, ld, FZ, FQ, in, o, cv, ypart, st);
-  };
-  auto rp = [&](const double* in, double* o) {
-    gm_bd<FT>(false, m, n, p, alpha, M, ld, FQ, in, o, cv[8], cv[9], ypart, st);
-  };
+  k_scal<<<nblk(p), KT, 0, st>>>(ra, w, p, out);
+  k_scal<<<nblk(n), KT, 0, st>>>(sa, o2, n, o2);
+  k_scal<<<nblk(m), KT, 0, st>>>(ra, o3, m, o3);
+}
+
+// left preconditioner for GLS (left_gls_apply, krylov.hpp:232-250)
+template <class FT>
+static void gm_left_gls(int n, int m, int p, double alpha, const FT* M, int64_t ld, const Fac<FT>& FZ,
+                        const Fac<FT>& FQ, const double* w, double* out, double* const* cv, double* ypart,
+                        cudaStream_t st) {
+  const double ia = 1.0 / alpha;
+  const int kk = std::min(n, p);
+  const Mask rqm{2, n - kk, m + (p - kk)};
+  double *t = cv[0], *q = cv[1], *h = cv[2], *g = cv[3], *u = cv[4];
+  // t = W^+T w3 = Q [R^-T w3; 0]
+  k_fill<double><<<nblk(n), KT, 0, st>>>(t, n, 0.0);
+  k_copy<double><<<nblk(m), KT, 0, st>>>(w + p + n, m, t);
+  trsv<FT, double>(M, ld, 0, 0, m, true, t, st);
+  apply_F<FT, double>(FZ, false, t, ypart, st);
+  // h = w1 - V^T t, V^T t = Z^T T^T Q^T t
+  k_copy<double><<<nblk(n), KT, 0, st>>>(t, n, q);
+  apply_F<FT, double>(FZ, true, q, ypart, st);
+  gemv_h<FT, double>(M, ld, 0, n, m, p, rqm, q, h, st);
+  apply_F<FT, double>(FQ, false, h, ypart, st);
+  k_sub<double><<<nblk(p), KT, 0, st>>>(w, h, p, h);
+  // g = w2 - (1/alpha) V h, V h = Q T Z h
+  k_copy<double><<<nblk(p), KT, 0, st>>>(h, p, u);
+  apply_F<FT, double>(FQ, true, u, ypart, st);
+  gemv_n<FT, double>(M, ld, 0, n, m, p, rqm, u, g, st);
+  apply_F<FT, double>(FZ, false, g, ypart, st);
+  k_scal<<<nblk(n), KT, 0, st>>>(-ia, g, n, g);
+  k_axpy<<<nblk(n), KT, 0, st>>>(1.0, w + p, n, g);
+  // o3 = W^+ g = R^-1 (Q^T g)(0:m)
+  apply_F<FT, double>(FZ, true, g, ypart, st);
+  trsv<FT, double>(M, ld, 0, 0, m, false, g, st);
+  k_scal<<<nblk(p), KT, 0, st>>>(ia, h, p, out);
+  k_copy<double><<<nblk(n), KT, 0, st>>>(t, n, out + p);
+  k_copy<double><<<nblk(m), KT, 0, st>>>(g, m, out + p + n);
+}
+
+// gls_correction_solve (Algorithm 3, gls.hpp:106-154) at binary64 on the widened
+// factors: (f1 p, f2 n, f3 m) -> (dy p, dz n, dx m)
+template <class FT>
+static void gm_cascade_gls(int n, int m, int p, const FT* M, int64_t ld, const Fac<FT>& FZ,
+                           const Fac<FT>& FQ, const double* f1, const double* f2, const double* f3,
+                           double* const* cv, double* ypart, double* dy, double* dz, double* dx,
+                           cudaStream_t st) {
+  const int nm = n - m, kp = p - n + m;
+  const int kk = std::min(n, p);
+  const Mask none{0, 0, 0};
+  const Mask rqm{2, n - kk, m + (p - kk)};
+  double *u = cv[0], *w = cv[1], *h1 = cv[2], *g2 = cv[3], *t4 = cv[4], *r2 = cv[5], *g = cv[6],
+         *r1v = cv[7], *tq = cv[8], *hh = cv[9];
+  k_copy<double><<<nblk(n), KT, 0, st>>>(f2, n, u);
+  k_copy<double><<<nblk(p), KT, 0, st>>>(f1, p, w);
+  k_copy<double><<<nblk(m), KT, 0, st>>>(f3, m, h1);
+  apply_F<FT, double>(FZ, true, u, ypart, st);                        // u = Q^T f2
+  apply_F<FT, double>(FQ, true, w, ypart, st);                        // w = Z f1
+  trsv<FT, double>(M, ld, 0, 0, m, true, h1, st);                     // R^T h1 = f3
+  k_copy<double><<<nblk(nm), KT, 0, st>>>(u + m, nm, g2);
+  trsv<FT, double>(M, ld, m, m + kp, nm, false, g2, st);              // T22 g2 = u2
+  gemv_h<FT, double>(M, ld, 0, m, m + kp, nm, none, h1, t4, st);       // T12^T h1
+  gemv_h<FT, double>(M, ld, 0, m, m, kp, rqm, h1, tq, st);             // T11^T h1
+  k_subsub<double><<<nblk(nm), KT, 0, st>>>(w + kp, g2, t4, nm, r2);  // w2 - g2 - T12^T h1
+  k_sub<double><<<nblk(kp), KT, 0, st>>>(w, tq, kp, g);               // g1 = w1 - T11^T h1
+  k_copy<double><<<nblk(nm), KT, 0, st>>>(g2, nm, g + kp);
+  trsv<FT, double>(M, ld, m, m + kp, nm, true, r2, st);               // T22^T h2 = ...
+  k_copy<double><<<nblk(p), KT, 0, st>>>(g, p, hh);
+  apply_F<FT, double>(FQ, false, hh, ypart, st);                       // dy = Z^T g
+  gemv_n<FT, double>(M, ld, 0, m, m, kp, rqm, g, t4, st);              // T11 g1
+  gemv_n<FT, double>(M, ld, 0, m, m + kp, nm, none, g2, tq, st);       // T12 g2
+  k_sub2<double><<<nblk(m), KT, 0, st>>>(u, t4, tq, m, r1v);          // u1 - (T11 g1 + T12 g2)
+  trsv<FT, double>(M, ld, 0, 0, m, false, r1v, st);                   // R dx = ...
+  k_copy<double><<<nblk(m), KT, 0, st>>>(h1, m, u);
+  k_copy<double><<<nblk(nm), KT, 0, st>>>(r2, nm, u + m);
+  apply_F<FT, double>(FZ, false, u, ypart, st);                        // Q [h1; h2]
+  k_copy<double><<<nblk(p), KT, 0, st>>>(hh, p, dy);
+  k_scal<<<nblk(n), KT, 0, st>>>(-1.0, u, n, dz);                      // dz = -Q h
+  k_copy<double><<<nblk(m), KT, 0, st>>>(r1v, m, dx);
+}
+
+// Full MGS-GMRES with Givens rotations (gmres, krylov.hpp:436-512; rel_tol
+// 1e-6, max_iter N) on the augmented system: `lp` is the left preconditioner
+// (or the split preconditioner's left half), `rp` the right half (kind 2);
+// the solution is added to wacc.  Basis vectors live on the device, the
+// Hessenberg column and the rotations on the host (one small D2H per step).
+template <class OP, class LP, class RP>
+static int gmres_core(int kind, int N, const double* rhs, double* wacc, const OP& op, const LP& lp,
+                      const RP& rp, double* t2, double* t3, double* t4, double* part, int nb, double* hdev,
+                      GmBuf& bas, int& cap, int64_t* its_out, cudaStream_t st) {
+  cudaError_t e;
   auto grow = [&](int need) -> cudaError_t {
     if (need <= cap) return cudaSuccess;
     int nc = cap ? cap : 32;
@@ -820,9 +960,9 @@ static int gmres_correction(int kind, int m, int n, int p, double alpha, const F
       if ((e = grow(k + 2))) return MLSB_ERR_CUDA;
       if (kind == 2) {
         rp(V(k), t3);
-        gm_op(m, n, p, alpha, gA, gB, lda, ldb, sA, sB, t3, t4, rpart, cpart, st);
+        op(t3, t4);
       } else {
-        gm_op(m, n, p, alpha, gA, gB, lda, ldb, sA, sB, V(k), t4, rpart, cpart, st);
+        op(V(k), t4);
       }
       lp(t4, t2);
       for (int i = 0; i <= k; ++i) {  // modified Gram-Schmidt
@@ -880,12 +1020,102 @@ static int gmres_correction(int kind, int m, int n, int p, double alpha, const F
     }
   }
   *its_out = its;
+  return MLSB_OK;
+}
+
+// One GMRES-IR correction for LSE (krylov.hpp:640-681): rhs from the residual
+// blocks, optional cascade initial guess (left), GMRES, and the state update.
+template <class FT>
+static int gmres_correction(int kind, int m, int n, int p, double alpha, const FT* M, int64_t ld,
+                            const Fac<FT>& FZ, const Fac<FT>& FQ, const double* gA, const double* gB,
+                            int64_t lda, int64_t ldb, double sA, double sB, const double* rout,
+                            const double* cout, double* sw, double* su, double* rhs, double* wacc,
+                            double* t1, double* t2, double* t3, double* t4, double* part, int nb,
+                            double* hdev, GmBuf& bas, int& cap, double* const* cv, double* ypart,
+                            double* rpart, double* cpart, int* flag, int64_t* its_out,
+                            cudaStream_t st) {
+  const int N = m + p + n;
+  const double sqa = sqrt(alpha);
+  cudaError_t e;
+  k_scal<<<nblk(m + p), KT, 0, st>>>(sqa, rout, m + p, rhs);
+  k_scal<<<nblk(n), KT, 0, st>>>(1.0 / sqa, cout, n, rhs + m + p);
+  k_fill<double><<<nblk(N), KT, 0, st>>>(wacc, N, 0.0);
+  auto op = [&](const double* in, double* o) {
+    gm_op(m, n, p, alpha, gA, gB, lda, ldb, sA, sB, in, o, rpart, cpart, st);
+  };
+  if (kind == 1) {  // cascade initial guess: the left preconditioner is singular on null(B)
+    gm_cascade<FT>(m, n, p, M, ld, FZ, FQ, rout, rout + m, cout, cv, ypart, t1, t1 + m, t1 + m + p, st);
+    k_scal<<<nblk(m), KT, 0, st>>>(1.0 / sqa, t1, m, wacc);
+    k_scal<<<nblk(p), KT, 0, st>>>(-1.0 / sqa, t1 + m, p, wacc + m);
+    k_scal<<<nblk(n), KT, 0, st>>>(sqa, t1 + m + p, n, wacc + m + p);
+    op(wacc, t2);
+    k_axpy<<<nblk(N), KT, 0, st>>>(-1.0, t2, N, rhs);
+  }
+  auto lp = [&](const double* in, double* o) {
+    if (kind == 2) gm_bd<FT>(true, m, n, p, alpha, M, ld, FQ, in, o, cv[8], cv[9], ypart, st);
+    else gm_left<FT>(m, n, p, alpha, M, ld, FZ, FQ, in, o, cv, ypart, st);
+  };
+  auto rp = [&](const double* in, double* o) {
+    gm_bd<FT>(false, m, n, p, alpha, M, ld, FQ, in, o, cv[8], cv[9], ypart, st);
+  };
+  if (int rc = gmres_core(kind, N, rhs, wacc, op, lp, rp, t2, t3, t4, part, nb, hdev, bas, cap, its_out, st))
+    return rc;
   // r += sqa w1, v -= sqa w2, x += w3 / sqa (krylov.hpp:677-679), then the finite check
   k_axpy<<<nblk(m), KT, 0, st>>>(sqa, wacc, m, sw);
   k_axpy<<<nblk(p), KT, 0, st>>>(-sqa, wacc + m, p, sw + m);
   k_add_div<<<nblk(n), KT, 0, st>>>(wacc + m + p, sqa, n, su);
   k_finite_flag<<<nblk(m + p), KT, 0, st>>>(sw, m + p, flag);
   k_finite_flag<<<nblk(n), KT, 0, st>>>(su, n, flag);
+  if ((e = cudaGetLastError())) return MLSB_ERR_CUDA;
+  return MLSB_OK;
+}
+
+// One GMRES-IR correction for GLS (krylov.hpp:750-771): rhs = [sqa f1; f2/sqa;
+// sqa f3]; left: the cascade's (dy, dz, dx) as initial guess; update
+// y += sqa w1, z -= w2/sqa, x += sqa w3.  Driver layout: su = [x (m); y (p)],
+// sw = z (n); residual blocks f1 = cout[m:], f2 = rout, f3 = cout[:m].
+template <class FT>
+static int gmres_correction_gls(int kind, int n, int m, int p, double alpha, const FT* M, int64_t ld,
+                                const Fac<FT>& FZ, const Fac<FT>& FQ, const double* gW, const double* gV,
+                                int64_t ldw, int64_t ldv, double sW, double sV, const double* rout,
+                                const double* cout, double* sw, double* su, double* rhs, double* wacc,
+                                double* t1, double* t2, double* t3, double* t4, double* part, int nb,
+                                double* hdev, GmBuf& bas, int& cap, double* const* cv, double* ypart,
+                                double* rpart, double* cpart, int* flag, int64_t* its_out,
+                                cudaStream_t st) {
+  const int N = p + n + m;
+  const double sqa = sqrt(alpha);
+  cudaError_t e;
+  k_scal<<<nblk(p), KT, 0, st>>>(sqa, cout + m, p, rhs);
+  k_scal<<<nblk(n), KT, 0, st>>>(1.0 / sqa, rout, n, rhs + p);
+  k_scal<<<nblk(m), KT, 0, st>>>(sqa, cout, m, rhs + p + n);
+  k_fill<double><<<nblk(N), KT, 0, st>>>(wacc, N, 0.0);
+  double* tmp = t1;  // [u3; u1] staging of the operator; t1 is free once the initial guess is folded in
+  auto op = [&](const double* in, double* o) {
+    gm_op_gls(n, m, p, alpha, gW, gV, ldw, ldv, sW, sV, in, o, tmp, rpart, cpart, st);
+  };
+  if (kind == 1) {  // the cascade supplies the dz component the left preconditioner cannot see
+    gm_cascade_gls<FT>(n, m, p, M, ld, FZ, FQ, cout + m, rout, cout, cv, ypart, t1, t1 + p, t1 + p + n, st);
+    k_scal<<<nblk(p), KT, 0, st>>>(1.0 / sqa, t1, p, wacc);
+    k_scal<<<nblk(n), KT, 0, st>>>(-sqa, t1 + p, n, wacc + p);
+    k_scal<<<nblk(m), KT, 0, st>>>(1.0 / sqa, t1 + p + n, m, wacc + p + n);
+    op(wacc, t2);
+    k_axpy<<<nblk(N), KT, 0, st>>>(-1.0, t2, N, rhs);
+  }
+  auto lp = [&](const double* in, double* o) {
+    if (kind == 2) gm_bd_gls<FT>(true, n, m, p, alpha, M, ld, FZ, in, o, cv[7], cv[8], cv[9], ypart, st);
+    else gm_left_gls<FT>(n, m, p, alpha, M, ld, FZ, FQ, in, o, cv, ypart, st);
+  };
+  auto rp = [&](const double* in, double* o) {
+    gm_bd_gls<FT>(false, n, m, p, alpha, M, ld, FZ, in, o, cv[7], cv[8], cv[9], ypart, st);
+  };
+  if (int rc = gmres_core(kind, N, rhs, wacc, op, lp, rp, t2, t3, t4, part, nb, hdev, bas, cap, its_out, st))
+    return rc;
+  k_axpy<<<nblk(p), KT, 0, st>>>(sqa, wacc, p, su + m);                  // y += sqa w1
+  k_add_div<<<nblk(n), KT, 0, st>>>(wacc + p, -sqa, n, sw);              // z -= w2 / sqa
+  k_axpy<<<nblk(m), KT, 0, st>>>(sqa, wacc + p + n, m, su);              // x += sqa w3
+  k_finite_flag<<<nblk(m + p), KT, 0, st>>>(su, m + p, flag);
+  k_finite_flag<<<nblk(n), KT, 0, st>>>(sw, n, flag);
   if ((e = cudaGetLastError())) return MLSB_ERR_CUDA;
   return MLSB_OK;
 }
@@ -900,7 +1130,9 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   const int m = int(P.m), n = int(P.n), p = int(P.p);
   // GMRES-IR is built for real LSE with m >= n (the first case of the split
   // preconditioner, krylov.hpp:259-269; the reference's configs C1, C3)
-  if (P.gmres && (!kGm || !lse || m < n)) return MLSB_ERR_UNSUPPORTED;
+  // GMRES-IR: LSE with m >= n (the first case of the LSE split preconditioner,
+  // krylov.hpp:259-269; the reference's configs C1, C3), GLS for both cases
+  if (P.gmres && (!kGm || (lse && m < n))) return MLSB_ERR_UNSUPPORTED;
   const int R = lse ? m + p : n, C = lse ? n : m + p;
   const int64_t ld = R;
   const int kq = lse ? p : std::min(n, p);  // RQ reflectors
@@ -1002,19 +1234,23 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
     memcpy(&v, &b, 8);
     return v == 0.0 ? 1.0 : v;
   };
-  const double sA = lowf ? asd(hb[0]) : 1.0, c1 = lowf ? asd(hb[2]) : 1.0;
+  double sA = lowf ? asd(hb[0]) : 1.0;
+  const double c1 = lowf ? asd(hb[2]) : 1.0;
   double sB = lowf ? asd(hb[1]) : 1.0;
   if (P.gmres) {
-    // gmres_refine_lse (krylov.hpp:562-566): s_B = s_A ||B||_F / ||A||_F balances the blocks
+    // the GMRES drivers balance the blocks by their Frobenius norms:
+    // LSE s_B = s_A ||B||_F / ||A||_F (krylov.hpp:558-563), GLS s_W = s_V ||W||_F / ||V||_F (:685-688)
     k_cast<FT, WT><<<grid, KT, 0, st>>>(gA, P.lda, rows1, cols1, 1.0, M, ld, parts);
     k_sum_parts<<<1, 32, 0, st>>>(parts, grid, nsum + 0);
-    k_cast<FT, WT><<<grid, KT, 0, st>>>(gB, P.ldb, rows2, cols2, 1.0, M + m, ld, parts + grid);
+    k_cast<FT, WT><<<grid, KT, 0, st>>>(gB, P.ldb, rows2, cols2, 1.0, lse ? M + m : M + int64_t(m) * ld, ld,
+                                        parts + grid);
     k_sum_parts<<<1, 32, 0, st>>>(parts + grid, grid, nsum + 1);
     double hr[2];
     cudaMemcpyAsync(hr, nsum, sizeof(hr), cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;
     const double nAr = hr[0] > 0 ? sqrt(hr[0]) : 1.0, nBr = hr[1] > 0 ? sqrt(hr[1]) : 1.0;
-    sB = sA * nBr / nAr;
+    if (lse) sB = sA * nBr / nAr;
+    else sA = sB * nAr / nBr;
   }
   const double c2 = lse ? sB * c1 / sA : c1;  // LSE c_d = s_B c_b / s_A ; GLS c_d
   // right-hand sides (exact division, lse.hpp:326-329)
@@ -1226,8 +1462,9 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       g_t4 = g_t3 + nv;
       g_part = g_t4 + nv;
       g_h = g_part + g_nb;
-      // alpha = alpha_scale * ||r0|| (krylov.hpp:613)
-      k_dot_part<<<g_nb, KT, 0, st>>>(sw, sw, m, g_part);
+      // alpha = alpha_scale * ||r0|| (LSE, krylov.hpp:613) | ||y0|| (GLS, :720)
+      if (lse) k_dot_part<<<g_nb, KT, 0, st>>>(sw, sw, m, g_part);
+      else k_dot_part<<<g_nb, KT, 0, st>>>(su + m, su + m, p, g_part);
       k_dot_final<<<1, 32, 0, st>>>(g_part, g_nb, g_h);
       double r2 = 0.0;
       cudaMemcpyAsync(&r2, g_h, 8, cudaMemcpyDeviceToHost, st);
@@ -1352,10 +1589,14 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
     if constexpr (kGm) {
       if (P.gmres) {
         int64_t its = 0;
-        int rc = gmres_correction(P.gmres, m, n, p, g_alpha, M, ld, FZ, FQ, gA, gB, P.lda, P.ldb, sA,
-                                  sB, rout, cout, sw, su, g_rhs, g_w, g_t1, g_t2, g_t3, g_t4, g_part,
-                                  g_nb, g_h, gbas, g_cap, cv, ypart, rpart, cpart, flags + 3, &its,
-                                  st);
+        int rc = lse ? gmres_correction(P.gmres, m, n, p, g_alpha, M, ld, FZ, FQ, gA, gB, P.lda, P.ldb, sA,
+                                        sB, rout, cout, sw, su, g_rhs, g_w, g_t1, g_t2, g_t3, g_t4, g_part,
+                                        g_nb, g_h, gbas, g_cap, cv, ypart, rpart, cpart, flags + 3, &its,
+                                        st)
+                     : gmres_correction_gls(P.gmres, n, m, p, g_alpha, M, ld, FZ, FQ, gA, gB, P.lda, P.ldb,
+                                            sA, sB, rout, cout, sw, su, g_rhs, g_w, g_t1, g_t2, g_t3, g_t4,
+                                            g_part, g_nb, g_h, gbas, g_cap, cv, ypart, rpart, cpart,
+                                            flags + 3, &its, st);
         if (rc) return rc;
         out->inner += its;
         continue;

@@ -12,7 +12,7 @@ host side, around the GPU solvers.
   fixed / scientific, fixed on a tie).
 
 Methods: ``"direct"``, ``"ir"`` (classical IR, mplse / mpgls) and, for LSE,
-``"gmres-left"`` / ``"gmres-bd"`` (GMRES-IR, gmres_refine_lse,
+``"gmres-left"`` / ``"gmres-bd"`` (GMRES-IR, gmres_refine_lse / gmres_refine_gls,
 inc/krylov.hpp:545-689).  GMRES-IR for GLS is not built on the GPU yet: it
 reports status ``"unsupported"``.
 """
@@ -243,18 +243,14 @@ def run_experiment(problem, spec: GeneratorSpec, method: str,
             rep.status = res.trace.status
             rep.iterations = res.trace.iterations
             rep.timing.update({k: float(res.trace.timing.get(k, 0.0)) for k in rep.timing})
-        elif lse:
-            res = api.gmres_refine_lse(problem, cfg,
-                                       precond="left" if method == "gmres-left" else "bd_split")
+        else:
+            gm = api.gmres_refine_lse if lse else api.gmres_refine_gls
+            res = gm(problem, cfg, precond="left" if method == "gmres-left" else "bd_split")
             st = res.state
             rep.status = res.trace.status
             rep.iterations = res.trace.iterations
             rep.inner_iterations = res.trace.inner_iterations
             rep.timing.update({k: float(res.trace.timing.get(k, 0.0)) for k in rep.timing})
-        else:
-            rep.status = "unsupported"
-            rep.timing["other"] = time.perf_counter() - t0
-            return rep
         if lse:
             A, B, b, d = (np.asarray(t) for t in (problem.A, problem.B, problem.b, problem.d))
             rep.metric1 = metric_err1_lse(A, B, b, d, np.asarray(st.x))

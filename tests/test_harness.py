@@ -146,4 +146,4 @@ def test_run_experiment_c1(gpu):
     assert rgls.status == "converged" and rgls.metric1 < 1e-13 and rgls.metric2 < 1e-10
     rgg = H.run_experiment(gpu.GlsProblem(W, V, dg), H.GeneratorSpec("gls", 100, 200, 150, 1e4, 2),
                            "gmres-bd", gpu.RefinementConfig(maxit=10))
-    assert rgg.status == "unsupported"
+    assert rgg.status == "converged" and rgg.inner_iterations >= 1 and rgg.metric2 < 1e-10

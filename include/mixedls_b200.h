@@ -130,8 +130,8 @@ int mlsb_gls_direct(const double* W, int64_t ldw, const double* V, int64_t ldv, 
  * alpha_scale * ||r0||, preconditioned by the binary32 GRQ factors widened to
  * binary64.  precond: MLSB_PRECOND_LEFT (krylov.hpp:209-230, with the
  * triangular cascade as initial guess) or MLSB_PRECOND_BD_SPLIT (two-sided,
- * krylov.hpp:253-287).  Built for u_f = low and m >= n (the split
- * preconditioner's first case); other inputs return MLSB_ERR_UNSUPPORTED.
+ * krylov.hpp:253-287, both the m >= n and the n > m case).  Built for
+ * u_f = low; other factor precisions return MLSB_ERR_UNSUPPORTED.
  * trace->inner_iterations = total GMRES iterations. */
 enum { MLSB_PRECOND_LEFT = 0, MLSB_PRECOND_BD_SPLIT = 1 };
 int mlsb_gmres_lse(const double* A, int64_t lda, const double* B, int64_t ldb, const double* b,

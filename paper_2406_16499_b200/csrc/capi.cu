@@ -710,8 +710,7 @@ int mlsb_gmres_lse(const double* A, int64_t lda, const double* B, int64_t ldb, c
   if (precond != MLSB_PRECOND_LEFT && precond != MLSB_PRECOND_BD_SPLIT)
     return fail(MLSB_ERR_INVALID_INPUT, "gmres: unknown preconditioner");
   if (!(alpha_scale > 0.0)) return fail(MLSB_ERR_INVALID_INPUT, "gmres: alpha_scale must be positive");
-  if (cfg->u_f != MLSB_LOW || m < n)
-    return fail(MLSB_ERR_UNSUPPORTED, "gmres: built for u_f = low and m >= n");
+  if (cfg->u_f != MLSB_LOW) return fail(MLSB_ERR_UNSUPPORTED, "gmres: built for u_f = low");
   if (int rc = check_device()) return rc;
   DevScope scope(exec);
   if (!scope.ok) return fail(MLSB_ERR_CUDA, "cudaSetDevice failed");

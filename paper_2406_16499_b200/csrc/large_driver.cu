@@ -653,13 +653,56 @@ static void gm_dot(const double* x, const double* y, int n, double* part, int nb
   k_dot_final<<<1, 32, 0, st>>>(part, nb, out);
 }
 
-// block-diagonal split preconditioner, m >= n (bd_lse_apply, krylov.hpp:253-287)
+// block-diagonal split preconditioner for LSE (bd_lse_apply, krylov.hpp:253-287):
+// m >= n through T1 = T(0:n, 0:n); n > m with U = [T1 T2; 0 I] and
+// Y = [T1(n-p:m, n-p:m) T2(n-p:m, :); 0 I] (k = m - (n - p)) applied blockwise
 template <class FT>
 static void gm_bd(bool left, int m, int n, int p, double alpha, const FT* M, int64_t ld,
                   const Fac<FT>& FQ, const double* w, double* out, double* ta, double* tb,
-                  double* ypart, cudaStream_t st) {
+                  double* ypart, cudaStream_t st, double* tc = nullptr) {
   const double ra = 1.0 / sqrt(alpha), sa = sqrt(alpha);
   const Mask up{1, 0, 0};
+  const Mask none{0, 0, 0};
+  if (n > m) {
+    const int d = n - m, q0 = n - p, k = m - q0;  // Y's leading block: rows/cols q0 .. m of T
+    double* o2 = out + m;
+    double* o3 = out + m + p;
+    if (left) {
+      // o2 = Y (R^-1 w2): top T1(q0:m, q0:m) v_t + T2(q0:m, :) v_b, bottom v_b
+      k_copy<double><<<nblk(p), KT, 0, st>>>(w + m, p, ta);
+      trsv<FT, double>(M, ld, m, n - p, p, false, ta, st);
+      gemv_n<FT, double>(M, ld, q0, k, q0, k, up, ta, o2, st);
+      gemv_n<FT, double>(M, ld, q0, k, m, d, none, ta + k, tc, st);
+      k_axpy<<<nblk(k), KT, 0, st>>>(1.0, tc, k, o2);
+      k_copy<double><<<nblk(d), KT, 0, st>>>(ta + k, d, o2 + k);
+      // o3 = U^-T (Q w3): top T1^T o_t = q_t, bottom q_b - T2^T o_t
+      k_copy<double><<<nblk(n), KT, 0, st>>>(w + m + p, n, tb);
+      apply_F<FT, double>(FQ, true, tb, ypart, st);
+      trsv<FT, double>(M, ld, 0, 0, m, true, tb, st);
+      gemv_h<FT, double>(M, ld, 0, m, m, d, none, tb, tc, st);
+      k_sub<double><<<nblk(d), KT, 0, st>>>(tb + m, tc, d, tb + m);
+      k_copy<double><<<nblk(n), KT, 0, st>>>(tb, n, o3);
+    } else {
+      // o2 = R^-T (Y^T w2): top T1(q0:m,q0:m)^T w_t, bottom T2(q0:m,:)^T w_t + w_b
+      gemv_h<FT, double>(M, ld, q0, k, q0, k, up, w + m, ta, st);
+      gemv_h<FT, double>(M, ld, q0, k, m, d, none, w + m, tc, st);
+      k_copy<double><<<nblk(d), KT, 0, st>>>(w + m + k, d, ta + k);
+      k_axpy<<<nblk(d), KT, 0, st>>>(1.0, tc, d, ta + k);
+      trsv<FT, double>(M, ld, m, n - p, p, true, ta, st);
+      k_copy<double><<<nblk(p), KT, 0, st>>>(ta, p, o2);
+      // o3 = Q^T (U^-1 w3): bottom w_b, top T1^-1 (w_t - T2 w_b)
+      k_copy<double><<<nblk(n), KT, 0, st>>>(w + m + p, n, tb);
+      gemv_n<FT, double>(M, ld, 0, m, m, d, none, tb + m, tc, st);
+      k_sub<double><<<nblk(m), KT, 0, st>>>(tb, tc, m, tb);
+      trsv<FT, double>(M, ld, 0, 0, m, false, tb, st);
+      apply_F<FT, double>(FQ, false, tb, ypart, st);
+      k_copy<double><<<nblk(n), KT, 0, st>>>(tb, n, o3);
+    }
+    k_scal<<<nblk(m), KT, 0, st>>>(ra, w, m, out);
+    k_scal<<<nblk(p), KT, 0, st>>>(ra, o2, p, o2);
+    k_scal<<<nblk(n), KT, 0, st>>>(sa, o3, n, o3);
+    return;
+  }
   if (left) {
     k_copy<double><<<nblk(p), KT, 0, st>>>(w + m, p, ta);
     trsv<FT, double>(M, ld, m, n - p, p, false, ta, st);                 // t = R^-1 w2
@@ -1052,11 +1095,11 @@ static int gmres_correction(int kind, int m, int n, int p, double alpha, const F
     k_axpy<<<nblk(N), KT, 0, st>>>(-1.0, t2, N, rhs);
   }
   auto lp = [&](const double* in, double* o) {
-    if (kind == 2) gm_bd<FT>(true, m, n, p, alpha, M, ld, FQ, in, o, cv[8], cv[9], ypart, st);
+    if (kind == 2) gm_bd<FT>(true, m, n, p, alpha, M, ld, FQ, in, o, cv[8], cv[9], ypart, st, cv[7]);
     else gm_left<FT>(m, n, p, alpha, M, ld, FZ, FQ, in, o, cv, ypart, st);
   };
   auto rp = [&](const double* in, double* o) {
-    gm_bd<FT>(false, m, n, p, alpha, M, ld, FQ, in, o, cv[8], cv[9], ypart, st);
+    gm_bd<FT>(false, m, n, p, alpha, M, ld, FQ, in, o, cv[8], cv[9], ypart, st, cv[7]);
   };
   if (int rc = gmres_core(kind, N, rhs, wacc, op, lp, rp, t2, t3, t4, part, nb, hdev, bas, cap, its_out, st))
     return rc;
@@ -1130,9 +1173,8 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   const int m = int(P.m), n = int(P.n), p = int(P.p);
   // GMRES-IR is built for real LSE with m >= n (the first case of the split
   // preconditioner, krylov.hpp:259-269; the reference's configs C1, C3)
-  // GMRES-IR: LSE with m >= n (the first case of the LSE split preconditioner,
-  // krylov.hpp:259-269; the reference's configs C1, C3), GLS for both cases
-  if (P.gmres && (!kGm || (lse && m < n))) return MLSB_ERR_UNSUPPORTED;
+  // GMRES-IR: LSE and GLS, both cases of the split preconditioners
+  if (P.gmres && !kGm) return MLSB_ERR_UNSUPPORTED;
   const int R = lse ? m + p : n, C = lse ? n : m + p;
   const int64_t ld = R;
   const int kq = lse ? p : std::min(n, p);  // RQ reflectors

@@ -48,10 +48,33 @@ def test_gmres_rescues_ill_conditioned(gpu, ref):
         assert abs(res.trace.iterations - rr.iterations) <= 1
 
 
-def test_gmres_unsupported_shapes(gpu):
-    A, B, b, d = G.lse_problem(20, 30, 15, 1e2, 1e1, 1)  # m < n
+@pytest.mark.parametrize("precond", ["bd_split", "left"])
+@pytest.mark.parametrize("shape,kappa", [((20, 30, 15), 1e2), ((60, 90, 50), 1e4), ((100, 130, 40), 1e3)])
+def test_gmres_lse_wide_parity(gpu, ref, precond, shape, kappa):
+    """n > m: the second case of the LSE split preconditioner (U = [T1 T2; 0 I],
+    Y = [T1(n-p:m, n-p:m) T2(n-p:m, :); 0 I], krylov.hpp:367-381)."""
+    m, n, p = shape
+    A, B, b, d = G.lse_problem(m, n, p, kappa, 1e1, seed=5 + m + n)
+    cfg = gpu.RefinementConfig(maxit=10)
+    res = gpu.gmres_refine_lse(gpu.LseProblem(A, B, b, d), cfg, precond=precond)
+    rr = ref.gmres_lse(A, B, b, d, maxit=10, precond=precond)
+    assert res.trace.status == rr.status, (res.trace, rr.status)
+    if rr.status != "converged":
+        assert abs(res.trace.iterations - rr.iterations) <= 1
+        return
+    kap = np.linalg.cond(np.vstack([A, B])) * 1e2
+    msgs = check_parity("lse", rel(res.state.x, rr.x), fwd_bound(m, n, p, kap),
+                        res.trace.iterations, rr.iterations,
+                        lse_backward(A, B, b, d, res.state.x, res.state.r, res.state.v),
+                        lse_backward(A, B, b, d, rr.x, rr.r, rr.v), res.trace.status, rr.status)
+    assert not msgs, msgs
+
+
+def test_gmres_unsupported_precision(gpu):
+    A, B, b, d = G.lse_problem(20, 10, 5, 1e2, 1e1, 1)
+    cfg = gpu.RefinementConfig(precisions=gpu.PrecisionConfig("working", "working"))
     with pytest.raises(gpu.Unsupported):
-        gpu.gmres_refine_lse(gpu.LseProblem(A, B, b, d))
+        gpu.gmres_refine_lse(gpu.LseProblem(A, B, b, d), cfg)
 
 
 # GMRES-IR for GLS (gmres_refine_gls, krylov.hpp:673-784): both cases of the

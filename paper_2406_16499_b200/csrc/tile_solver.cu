@@ -258,7 +258,9 @@ __device__ void qr_stage(FT* M, int ld, int rend, int k, int cend, FT* tau, int 
     const FT tj = tau[j];
     const FT* v = M + size_t(j) * ld;
     int c = j + 1 + ((warp - (j + 1)) % NW + NW) % NW;
-    for (; c < cend; c += NW) {
+    // the owner's column j+1 first (it feeds the next reflector), then the
+    // warp's other columns four at a time so their warp sums overlap
+    if (c == j + 1 && c < cend) {
       FT* cc = M + size_t(c) * ld;
       if (tj != FT(0)) {
         FT s = FT(0);
@@ -269,7 +271,35 @@ __device__ void qr_stage(FT* M, int ld, int rend, int k, int cend, FT* tau, int 
         if (lane == 0) cc[j] -= s;
         for (int i = j + 1 + lane; i < rend; i += 32) cc[i] -= s * v[i];
       }
-      if (c == j + 1 && c < k) gen_col_reflector(cc, c, rend, &tau[c], lane);
+      if (c < k) gen_col_reflector(cc, c, rend, &tau[c], lane);
+      c += NW;
+    }
+    if (tj != FT(0)) {
+      for (; c < cend; c += 4 * NW) {
+        FT s[4] = {FT(0), FT(0), FT(0), FT(0)};
+        FT* cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cc[u] = M + size_t(min(c + u * NW, cend - 1)) * ld;
+        for (int i = j + 1 + lane; i < rend; i += 32) {
+          const FT vi = v[i];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) s[u] += vi * cc[u][i];
+        }
+        FT cj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          s[u] = warp_sum(s[u]);
+          cj[u] = cc[u][j];
+        }
+        __syncwarp();  // every lane has read cc[u][j] before lane 0 rewrites it
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (c + u * NW >= cend) break;
+          const FT su = (s[u] + cj[u]) * tj;
+          if (lane == 0) cc[u][j] = cj[u] - su;
+          for (int i = j + 1 + lane; i < rend; i += 32) cc[u][i] -= su * v[i];
+        }
+      }
     }
   }
   __syncthreads();
@@ -311,13 +341,26 @@ __device__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, int cc, FT* tau,
     __syncthreads();
     const FT tj = tau[j];
     if (tj != FT(0)) {
-      for (int i = tid; i < row; i += NT) {
-        FT* arow = M + i + size_t(c0) * ld;
+      // 4 threads per row (adjacent lanes), each with a quarter of the row's
+      // dot: chains of ~pc/4 FMAs instead of pc, every thread of the CTA busy;
+      // the quarters are combined as (q0 + q1) + (q2 + q3) (same in every lane)
+      const int qc = (pc + 3) / 4, c = lane & 3, r8 = lane >> 2;
+      const int qa = min(pc, c * qc), qb = min(pc, qa + qc);
+      for (int i0 = 0; i0 < row; i0 += NT / 4) {
+        const int i = i0 + warp * 8 + r8;
+        const bool ok = i < row;
+        FT* arow = M + (ok ? i : 0) + size_t(c0) * ld;
         FT w = FT(0);
-        for (int q = 0; q < pc; ++q) w += vrow[size_t(q) * ld] * arow[size_t(q) * ld];
-        w += arow[size_t(pc) * ld];
-        for (int q = 0; q < pc; ++q) arow[size_t(q) * ld] -= (tj * vrow[size_t(q) * ld]) * w;
-        arow[size_t(pc) * ld] -= tj * w;
+        const FT apc = ok ? arow[size_t(pc) * ld] : FT(0);
+        if (ok)
+          for (int q = qa; q < qb; ++q) w += vrow[size_t(q) * ld] * arow[size_t(q) * ld];
+        w += __shfl_xor_sync(0xffffffffu, w, 1);
+        w += __shfl_xor_sync(0xffffffffu, w, 2);
+        w += apc;
+        if (ok) {
+          for (int q = qa; q < qb; ++q) arow[size_t(q) * ld] -= (tj * vrow[size_t(q) * ld]) * w;
+          if (c == 0) arow[size_t(pc) * ld] = apc - tj * w;
+        }
       }
     }
     if (tid == 0) vrow[size_t(pc) * ld] = FT(scal[S_BETA]);

@@ -8,5 +8,5 @@ timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_c4.json 2> g
 tail -1 gpurun_out/bench_c4.json
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_rc=$?
 tail -1 gpurun_out/bench_ref.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/c4_launches.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:"lse_reg_kernel|fma_burn" --log-file gpurun_out/c4_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo launch_rc=$?

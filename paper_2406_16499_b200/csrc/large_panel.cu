@@ -548,6 +548,242 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelArgs<float> a) {
   cluster_barrier();
 }
 
+template <int RPT, int NT>
+__global__ void __launch_bounds__(NT, 1) panel_reg_kernel_c(PanelArgs<cf> a) {
+  constexpr int NW = NT / 32;
+  __shared__ cf wpart[NW][NB];
+  __shared__ double wnorm[NW];
+  __shared__ __align__(16) cf prow_s[NB];
+  __shared__ __align__(16) cf xd[2][PCL][NB];  // [parity][rank] CTA partials of d
+  __shared__ __align__(16) cf xp[2][NB];       // [parity] pivot row (from its owner CTA)
+  __shared__ double xn[2][PCL];                   // [parity][rank] CTA partials of ||x||^2
+  __shared__ __align__(8) unsigned long long xbar[2];  // exchange arrivals, per parity
+  __shared__ uint32_t rbase[PCL];                      // cluster address of xd in CTA c
+  __shared__ __align__(16) cf coef_s[NB];
+  __shared__ cf scal[2];
+  __shared__ cf G[NB * NB];
+  __shared__ cf taus[NB];
+
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = int(cl.block_rank()), ncl = a.ncl;
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int nb = a.nb;
+  const int rb = rank * a.rc, re = min(a.L, rb + a.rc);
+
+  cf P[RPT][NB];
+  int row[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    row[i] = rb + tid + NT * i;
+    const bool own = row[i] < re;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) P[i][k] = (own && k < nb) ? ld_view(a, row[i], k) : zero<cf>();
+    if (!own) row[i] = -1;  // never > q, never == q
+  }
+  for (int e = tid; e < NB * NB; e += NT) G[e] = zero<cf>();
+  const uint32_t xd0 = uint32_t(__cvta_generic_to_shared(&xd[0][0][0]));
+  if (tid < PCL) rbase[tid] = tid < ncl ? cl_addr(&xd[0][0][0], tid) : 0u;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(uint32_t(__cvta_generic_to_shared(&xbar[0]))));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(uint32_t(__cvta_generic_to_shared(&xbar[1]))));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster_barrier();  // every exchange barrier initialised before any remote signal
+  const uint32_t xbytes = uint32_t(ncl) * (NB * sizeof(cf) + sizeof(double)) + NB * sizeof(cf);
+  // exchange buffers and barrier as offsets from xd (the same in every CTA)
+  const uint32_t off_d = uint32_t(__cvta_generic_to_shared(&xd[0][rank][0])) - xd0;
+  const uint32_t off_p = uint32_t(__cvta_generic_to_shared(&xp[0][0])) - xd0;
+  const uint32_t off_n = uint32_t(__cvta_generic_to_shared(&xn[0][rank])) - xd0;
+  const uint32_t off_bar = uint32_t(__cvta_generic_to_shared(&xbar[0])) - xd0;
+  constexpr uint32_t par_d = sizeof(xd[0]), par_p = sizeof(xp[0]), par_n = sizeof(xn[0]);
+
+  // Rotating frame: at step q, P[i][f] holds column (q + f) mod NB, so the
+  // current column is always P[i][0] and the step is the same code for every
+  // q (a real loop: the unrolled 32-step body does not fit the i-cache).
+#pragma unroll 1
+  for (int q = 0; q < nb; ++q) {
+    const int par = q & 1;
+    long long* pq = (a.probe && rank == 0 && tid == 0) ? a.probe + 8 * q : nullptr;
+    if (pq) pq[0] = clock64();
+    // ---- 1. thread partials (frame order)
+    cf d[NB];
+#pragma unroll
+    for (int f = 0; f < NB; ++f) d[f] = zero<cf>();
+    double nn = 0.0;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      if (row[i] > q) {
+        const cf x = P[i][0];
+        nn += abs2d(x);
+        const cf xc = conj_(x);
+#pragma unroll
+        for (int f = 0; f < NB; ++f) mac(d[f], xc, P[i][f]);
+      } else if (row[i] == q) {
+#pragma unroll
+        for (int f = 0; f < NB; ++f) prow_s[f] = P[i][f];
+      }
+    }
+    // ---- 2. warp transposed reduction: lane l ends with the warp sum of d[l]
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const bool up = (l & s) != 0;
+#pragma unroll
+      for (int j = 0; j < s; ++j) {
+        const cf send = up ? d[j] : d[j + s];
+        const cf keep = up ? d[j + s] : d[j];
+        d[j] = keep + cf{__shfl_xor_sync(0xffffffffu, send.x, s), __shfl_xor_sync(0xffffffffu, send.y, s)};
+      }
+    }
+    nn = wsum(nn);
+    wpart[w][l] = d[0];
+    if (l == 0) wnorm[w] = nn;
+    if (pq) pq[1] = clock64();
+    __syncthreads();
+    if (pq) pq[2] = clock64();
+    // ---- 3. CTA partials pushed into slot [rank] of every CTA's exchange
+    //         buffer by st.async, each landing store counted on the
+    //         destination's mbarrier (no fence, no cluster barrier)
+    if (tid == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       uint32_t(__cvta_generic_to_shared(&xbar[par]))),
+                   "r"(xbytes)
+                   : "memory");
+    {
+      // one 16-byte chunk (two complex values) per (destination, chunk) pair:
+      // threads u = 16 c + j
+      const uint32_t bo = off_bar + 8 * par;
+      for (int u = tid; u < 16 * ncl; u += NT) {
+        const int c = u >> 4, j = u & 15;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) {
+          const float4 t = *reinterpret_cast<const float4*>(&wpart[ww][2 * j]);
+          v.x += t.x, v.y += t.y, v.z += t.z, v.w += t.w;
+        }
+        st_async(rbase[c] + off_d + par * par_d + 16 * j, v, rbase[c] + bo);
+      }
+      if (q >= rb && q < re)  // this CTA owns the pivot row
+        for (int u = tid; u < 16 * ncl; u += NT) {
+          const int c = u >> 4, j = u & 15;
+          st_async(rbase[c] + off_p + par * par_p + 16 * j, *reinterpret_cast<const float4*>(&prow_s[2 * j]),
+                   rbase[c] + bo);
+        }
+      if (tid < ncl) {
+        double t[NW];
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) t[ww] = wnorm[ww];
+        double v = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) v += t[ww];
+        st_async(rbase[tid] + off_n + par * par_n, v, rbase[tid] + bo);
+      }
+    }
+    // ---- 4. warp 0: totals in rank order (lane f: d_f, p_f), xLARFG, the
+    //         update coefficients coef_f = tau v^T P[:, f] and Gram entries
+    if (pq) pq[3] = clock64();
+    if (w == 0) {
+      mbar_wait(&xbar[par], (q >> 1) & 1);
+      if (pq) pq[4] = clock64();
+      cf td[PCL];
+      double tn[PCL];
+#pragma unroll
+      for (int c = 0; c < PCL; ++c) {
+        const bool in = c < ncl;
+        td[c] = in ? xd[par][c][l] : zero<cf>();
+        tn[c] = in ? xn[par][c] : 0.0;
+      }
+      const cf pk = xp[par][l];
+#pragma unroll
+      for (int h = PCL / 2; h >= 1; h >>= 1)
+#pragma unroll
+        for (int c = 0; c < h; ++c) {
+          td[c] = td[c] + td[c + h];
+          tn[c] += tn[c + h];
+        }
+      const cf dk = td[0];
+      const double nrm = tn[0];
+      cf tau, inv, beta;
+      larfg_s(cf{__shfl_sync(0xffffffffu, pk.x, 0), __shfl_sync(0xffffffffu, pk.y, 0)}, nrm, tau, inv, beta);
+      const cf sv = pk + conj_(inv) * dk;  // v^H P[:, f]
+      coef_s[l] = (l >= 1 && l < nb - q) ? conj_(tau) * sv : zero<cf>();  // H^H = I - conj(tau) v v^H
+      if (l >= NB - q) G[(q + l - NB) + NB * q] = conj_(pk) + inv * conj_(dk);  // v_k^H v_q
+      if (l == 0) {
+        scal[0] = inv;
+        scal[1] = beta;
+        taus[q] = tau;
+      }
+    }
+    if (pq) pq[5] = clock64();
+    __syncthreads();
+    if (pq) pq[6] = clock64();
+    // ---- 5. rank-1 update of my rows, in registers, then rotate the frame
+    const cf inv = scal[0], beta = scal[1];
+    cf v[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) v[i] = row[i] == q ? one<cf>() : (row[i] > q ? inv * P[i][0] : zero<cf>());
+#pragma unroll
+    for (int f2 = 0; f2 < NB; f2 += 2) {
+      const float4 c4 = *reinterpret_cast<const float4*>(&coef_s[f2]);
+      const cf cc[2] = {cf{c4.x, c4.y}, cf{c4.z, c4.w}};
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        if (f2 + t >= 1)
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) P[i][f2 + t] = P[i][f2 + t] - cc[t] * v[i];
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const cf p0 = row[i] == q ? beta : (row[i] > q ? v[i] : P[i][0]);
+#pragma unroll
+      for (int f = 0; f < NB - 1; ++f) P[i][f] = P[i][f + 1];
+      P[i][NB - 1] = p0;
+    }
+    if (pq) pq[7] = clock64();
+  }
+  __syncthreads();
+  // ---- write back the factored panel and the dense reflector block; frame
+  //      index f holds column (nb + f) mod NB after nb steps
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int r = row[i];
+    if (r < 0) continue;
+    const int64_t vi = a.rq ? (a.c0 - r - a.vbase) : r;
+#pragma unroll
+    for (int f = 0; f < NB; ++f) {
+      const int k = (nb + f) & (NB - 1);
+      if (k < nb) {
+        st_view(a, r, k, P[i][f]);
+        a.V[vi + k * a.ldv] = r < k ? zero<cf>() : (r == k ? one<cf>() : P[i][f]);
+      }
+    }
+  }
+  if (rank == 0) {
+    if (tid < nb) a.tau[tid] = taus[tid];
+    if (w == 0) {
+      // T[q][q] = tau_q ; T[0:q, q] = -tau_q T[0:q, 0:q] G[0:q, q]; lane l owns row l
+      cf Tr[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) Tr[k] = zero<cf>();
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        if (q < nb) {
+          cf t = zero<cf>();
+#pragma unroll
+          for (int k = 0; k < NB; ++k)
+            if (k < q) mac(t, Tr[k], G[k + NB * q]);
+          const cf tq = taus[q];
+          Tr[q] = l < q ? -(tq * t) : (l == q ? tq : zero<cf>());
+        }
+      }
+      if (l < nb)
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+          if (q < nb) a.Tm[l + q * NB] = Tr[q];
+    }
+  }
+  cluster_barrier();
+}
+
 template <class T>
 static size_t panel_smem(int rc) {
   const int NV = 2 * NB;
@@ -611,6 +847,25 @@ cudaError_t panel_factor(T* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb
       cfg.dynamicSmemBytes = 0;
       attr[0].val.clusterDim.x = ncl;
       return cudaLaunchKernelEx(&cfg, kern, a);
+    }
+  }
+  if constexpr (std::is_same<T, cf>::value) {
+    // complex64: 128 threads x 2 rows per CTA while 16 CTAs hold the panel
+    if (L <= PCL * 128 * 2 && !smem_panel) {
+      const int ncl = std::min(PCL, (L + 255) / 256);
+      a.ncl = ncl;
+      a.rc = (L + ncl - 1) / ncl;
+      static bool attr_c = false;
+      if (!attr_c) {
+        if ((e = cudaFuncSetAttribute(panel_reg_kernel_c<2, 128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)))
+          return e;
+        attr_c = true;
+      }
+      cfg.gridDim = dim3(ncl);
+      cfg.blockDim = dim3(128);
+      cfg.dynamicSmemBytes = 0;
+      attr[0].val.clusterDim.x = ncl;
+      return cudaLaunchKernelEx(&cfg, panel_reg_kernel_c<2, 128>, a);
     }
   }
   const size_t sm = panel_smem<T>(a.rc);

@@ -1696,9 +1696,13 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       k_demote<WT, CT><<<nblk(n), KT, 0, st>>>(rout, n, sb, u);       // f2
       k_demote<WT, CT><<<nblk(p), KT, 0, st>>>(cout + m, p, sb, w);   // f1
       k_demote<WT, CT><<<nblk(m), KT, 0, st>>>(cout, m, sb, h1);      // f3
+      mark("demote");
       apply_F<FT, CT>(FZ, true, u, ypart, st);                        // u = Q^H f2
+      mark("applyQh");
       apply_F<FT, CT>(FQ, true, w, ypart, st);                        // w = Z f1 = F^H f1
+      mark("applyZ");
       trsv<FT, CT>(M, ld, 0, 0, m, true, h1, st);                     // R^H h1 = f3
+      mark("trsvRh");
       k_copy<CT><<<nblk(nm), KT, 0, st>>>(u + m, nm, g2);
       trsv<FT, CT>(M, ld, m, m + kp, nm, false, g2, st);              // T22 g2 = u2
       gemv_h<FT, CT>(M, ld, 0, m, m + kp, nm, none, h1, t4, st);       // T12^H h1
@@ -1706,16 +1710,22 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       k_subsub<CT><<<nblk(nm), KT, 0, st>>>(w + kp, g2, t4, nm, r2);  // w2 - g2 - T12^H h1
       k_sub<CT><<<nblk(kp), KT, 0, st>>>(w, tq, kp, g);               // g1 = w1 - T11^H h1
       k_copy<CT><<<nblk(nm), KT, 0, st>>>(g2, nm, g + kp);
+      mark("T22+gemv");
       trsv<FT, CT>(M, ld, m, m + kp, nm, true, r2, st);               // T22^H h2 = ...
       k_copy<CT><<<nblk(p), KT, 0, st>>>(g, p, hh);
+      mark("trsvT22h");
       apply_F<FT, CT>(FQ, false, hh, ypart, st);                       // dy = Z^H g = F g
+      mark("applyZh");
       gemv_n<FT, CT>(M, ld, 0, m, m, kp, rqm, g, t4, st);              // T11 g1
       gemv_n<FT, CT>(M, ld, 0, m, m + kp, nm, none, g2, tq, st);       // T12 g2
       k_sub2<CT><<<nblk(m), KT, 0, st>>>(u, t4, tq, m, r1v);          // u1 - (T11 g1 + T12 g2)
+      mark("gemv_n x2");
       trsv<FT, CT>(M, ld, 0, 0, m, false, r1v, st);                   // R dx = ...
+      mark("trsvR");
       k_copy<CT><<<nblk(m), KT, 0, st>>>(h1, m, u);
       k_copy<CT><<<nblk(nm), KT, 0, st>>>(r2, nm, u + m);
       apply_F<FT, CT>(FZ, false, u, ypart, st);                        // Q [h1; h2]
+      mark("applyQ");
       k_promote_add<WT, CT><<<nblk(m), KT, 0, st>>>(su, m, r1v, sb, false, flags + 3);
       k_promote_add<WT, CT><<<nblk(p), KT, 0, st>>>(su + m, p, hh, sb, false, flags + 3);
       k_promote_add<WT, CT><<<nblk(n), KT, 0, st>>>(sw, n, u, sb, true, flags + 3);  // dz = -Q h

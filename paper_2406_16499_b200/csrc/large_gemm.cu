@@ -150,13 +150,15 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, T alpha,
 // along the operand's contiguous dimension when pointer and leading dimension
 // allow it (VEC), staged in registers while the previous tile is consumed,
 // and transposed into the k-major shared layout on the store.
-template <bool HA, bool HB, bool VEC>
+template <bool HA, bool HB, bool VEC, int BK>
 __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, const float* __restrict__ A,
                                               int64_t lda, const float* __restrict__ B, int64_t ldb,
                                               float beta, float* __restrict__ C, int64_t ldc, int kchunk,
                                               int64_t split_stride, int bx, int by, int bz,
-                                              float (&As)[2][16][132], float (&Bs)[2][16][132]) {
-  constexpr int BM = 128, BN = 128, BK = 16;
+                                              float (*As)[BK][132], float (*Bs)[BK][132]) {
+  constexpr int BM = 128, BN = 128;
+  constexpr int KQ = BK / 4;           // float4 slots along k for the k-contiguous operands
+  constexpr int NPART = BK / 16;       // staging parts per operand (2 float4 slots each)
   const int tid = threadIdx.x, tr = tid & 15, tc = tid >> 4;
   const int i0 = bx * BM, j0 = by * BN;
   const int kbeg = bz * kchunk;
@@ -166,10 +168,10 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
   // staging: 512 float4 slots per operand tile, two per thread
   float ra[8], rb[8];
   // op(A)(i,k): !HA -> A[i + k lda] (contiguous in i) ; HA -> A[k + i lda] (contiguous in k)
-  auto load_a = [&](int k0) {
+  auto load_a = [&](int k0, int part) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      const int slot = tid + 256 * s;
+      const int slot = tid + 256 * (2 * part + s);
       if (!HA) {  // 4 consecutive rows i of one k
         const int i = (slot & 31) * 4, k = slot >> 5;
         const int gi = i0 + i, gk = k0 + k;
@@ -183,7 +185,7 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
             ra[4 * s + t] = (gk < kend && gi + t < M) ? A[gi + t + int64_t(gk) * lda] : 0.f;
         }
       } else {  // 4 consecutive k of one row i
-        const int k = (slot & 3) * 4, i = slot >> 2;
+        const int k = (slot % KQ) * 4, i = slot / KQ;
         const int gi = i0 + i, gk = k0 + k;
         if (VEC) {
           float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -198,10 +200,10 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
     }
   };
   // op(B)(k,j): !HB -> B[k + j ldb] (contiguous in k) ; HB -> B[j + k ldb] (contiguous in j)
-  auto load_b = [&](int k0) {
+  auto load_b = [&](int k0, int part) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      const int slot = tid + 256 * s;
+      const int slot = tid + 256 * (2 * part + s);
       if (HB) {
         const int j = (slot & 31) * 4, k = slot >> 5;
         const int gj = j0 + j, gk = k0 + k;
@@ -215,7 +217,7 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
             rb[4 * s + t] = (gk < kend && gj + t < N) ? B[gj + t + int64_t(gk) * ldb] : 0.f;
         }
       } else {
-        const int k = (slot & 3) * 4, j = slot >> 2;
+        const int k = (slot % KQ) * 4, j = slot / KQ;
         const int gj = j0 + j, gk = k0 + k;
         if (VEC) {
           float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -234,29 +236,29 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
   for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
-  auto store_a = [&](int buf) {
+  auto store_a = [&](int buf, int part) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      const int slot = tid + 256 * s;
+      const int slot = tid + 256 * (2 * part + s);
       if (!HA) {
         const int i = (slot & 31) * 4, k = slot >> 5;
         *reinterpret_cast<float4*>(&As[buf][k][i]) = make_float4(ra[4 * s], ra[4 * s + 1], ra[4 * s + 2], ra[4 * s + 3]);
       } else {
-        const int k = (slot & 3) * 4, i = slot >> 2;
+        const int k = (slot % KQ) * 4, i = slot / KQ;
 #pragma unroll
         for (int t = 0; t < 4; ++t) As[buf][k + t][i] = ra[4 * s + t];
       }
     }
   };
-  auto store_b = [&](int buf) {
+  auto store_b = [&](int buf, int part) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      const int slot = tid + 256 * s;
+      const int slot = tid + 256 * (2 * part + s);
       if (HB) {
         const int j = (slot & 31) * 4, k = slot >> 5;
         *reinterpret_cast<float4*>(&Bs[buf][k][j]) = make_float4(rb[4 * s], rb[4 * s + 1], rb[4 * s + 2], rb[4 * s + 3]);
       } else {
-        const int k = (slot & 3) * 4, j = slot >> 2;
+        const int k = (slot % KQ) * 4, j = slot / KQ;
 #pragma unroll
         for (int t = 0; t < 4; ++t) Bs[buf][k + t][j] = rb[4 * s + t];
       }
@@ -279,26 +281,35 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
 
   int buf = 0;
   if (kbeg < kend) {
-    load_a(kbeg);
-    store_a(0);
-    load_b(kbeg);
-    store_b(0);
+#pragma unroll
+    for (int pt = 0; pt < NPART; ++pt) {
+      load_a(kbeg, pt);
+      store_a(0, pt);
+      load_b(kbeg, pt);
+      store_b(0, pt);
+    }
   }
   __syncthreads();
-  // the next tile is staged half at a time (A during kk 0..7, B during kk
-  // 8..15) so only 8 staging registers are live
+  // the next tile is staged a part at a time (2 float4 slots per thread per
+  // window of 8 kk steps: A parts first, then B parts), so only 8 staging
+  // registers are live
   for (int k0 = kbeg; k0 < kend; k0 += BK) {
     const bool more = k0 + BK < kend;
-    if (more) load_a(k0 + BK);
 #pragma unroll
-    for (int kk = 0; kk < BK / 2; ++kk) step(buf, kk);
-    if (more) {
-      store_a(buf ^ 1);
-      load_b(k0 + BK);
+    for (int win = 0; win < 2 * NPART; ++win) {
+      const bool isA = win < NPART;
+      const int pt = isA ? win : win - NPART;
+      if (more) {
+        if (isA) load_a(k0 + BK, pt);
+        else load_b(k0 + BK, pt);
+      }
+#pragma unroll
+      for (int kk = 8 * win; kk < 8 * win + 8; ++kk) step(buf, kk);
+      if (more) {
+        if (isA) store_a(buf ^ 1, pt);
+        else store_b(buf ^ 1, pt);
+      }
     }
-#pragma unroll
-    for (int kk = BK / 2; kk < BK; ++kk) step(buf, kk);
-    if (more) store_b(buf ^ 1);
     __syncthreads();
     buf ^= 1;
   }
@@ -336,19 +347,20 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
 // Persistent form: the grid may be smaller than the tile count (gm x gn x gz),
 // each CTA walking tiles with a stride, so a trailing update can leave SMs
 // free for the look-ahead stream's panel cluster and small GEMMs.
-template <bool HA, bool HB, bool VEC>
+template <bool HA, bool HB, bool VEC, int BK>
 __global__ void __launch_bounds__(256, 2) sgemm128(int M, int N, int K, float alpha,
                                                    const float* __restrict__ A, int64_t lda,
                                                    const float* __restrict__ B, int64_t ldb, float beta,
                                                    float* __restrict__ C, int64_t ldc, int kchunk,
                                                    int64_t split_stride, int gm, int gn, int gz) {
-  __shared__ __align__(16) float As[2][16][132];
-  __shared__ __align__(16) float Bs[2][16][132];
+  extern __shared__ __align__(16) unsigned char gsm_[];
+  float(*As)[BK][132] = reinterpret_cast<float(*)[BK][132]>(gsm_);
+  float(*Bs)[BK][132] = reinterpret_cast<float(*)[BK][132]>(gsm_ + sizeof(float) * 2 * BK * 132);
   const int ntiles = gm * gn * gz;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int bx = t % gm, by = (t / gm) % gn, bz = t / (gm * gn);
-    sgemm128_tile<HA, HB, VEC>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, split_stride, bx, by, bz,
-                               As, Bs);
+    sgemm128_tile<HA, HB, VEC, BK>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, split_stride, bx, by,
+                                   bz, As, Bs);
     __syncthreads();
   }
 }
@@ -434,6 +446,31 @@ static cudaError_t gemm_tile(bool ha, bool hb, int M, int N, int K, T alpha, con
 static thread_local int g_gemm_cta_cap = 0;
 void set_gemm_cta_cap(int cap) { g_gemm_cta_cap = cap; }
 
+constexpr int GBK = 32;  // k-tile of the binary32 WY GEMM (MLSB_GEMM_BK16=1: 16)
+template <bool VEC, int BK>
+static void launch128_bk(bool ha, bool hb, int grid, int gm, int gn, int gz, int M, int N, int K, float alpha,
+                         const float* A, int64_t lda, const float* B, int64_t ldb, float beta, float* C,
+                         int64_t ldc, int kchunk, int64_t sstr, cudaStream_t st) {
+  constexpr size_t sm = sizeof(float) * 4 * BK * 132;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sgemm128<false, false, VEC, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    cudaFuncSetAttribute(sgemm128<true, false, VEC, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    cudaFuncSetAttribute(sgemm128<false, true, VEC, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    cudaFuncSetAttribute(sgemm128<true, true, VEC, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    attr = true;
+  }
+  if (!ha && !hb)
+    sgemm128<false, false, VEC, BK><<<grid, 256, sm, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, gm, gn, gz);
+  else if (ha && !hb)
+    sgemm128<true, false, VEC, BK><<<grid, 256, sm, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, gm, gn, gz);
+  else if (!ha && hb)
+    sgemm128<false, true, VEC, BK><<<grid, 256, sm, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, gm, gn, gz);
+  else
+    sgemm128<true, true, VEC, BK><<<grid, 256, sm, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, gm, gn, gz);
+}
+
+
 template <bool VEC>
 static void launch128(bool ha, bool hb, dim3 tiles, int M, int N, int K, float alpha, const float* A,
                       int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc,
@@ -441,18 +478,11 @@ static void launch128(bool ha, bool hb, dim3 tiles, int M, int N, int K, float a
   const int nt = int(tiles.x * tiles.y * tiles.z);
   const int grid = g_gemm_cta_cap > 0 ? std::min(nt, g_gemm_cta_cap) : nt;
   const int gm = int(tiles.x), gn = int(tiles.y), gz = int(tiles.z);
-  if (!ha && !hb)
-    sgemm128<false, false, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr,
-                                                   gm, gn, gz);
-  else if (ha && !hb)
-    sgemm128<true, false, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr,
-                                                   gm, gn, gz);
-  else if (!ha && hb)
-    sgemm128<false, true, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr,
-                                                   gm, gn, gz);
+  static const bool bk16 = getenv("MLSB_GEMM_BK16") != nullptr;
+  if (bk16)
+    launch128_bk<VEC, 16>(ha, hb, grid, gm, gn, gz, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, st);
   else
-    sgemm128<true, true, VEC><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr,
-                                                   gm, gn, gz);
+    launch128_bk<VEC, GBK>(ha, hb, grid, gm, gn, gz, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, st);
 }
 
 static cudaError_t sgemm_sq(bool ha, bool hb, int M, int N, int K, float alpha, const float* A, int64_t lda,
@@ -467,7 +497,7 @@ static cudaError_t sgemm_sq(bool ha, bool hb, int M, int N, int K, float alpha, 
       splits *= 2;
   }
   int kchunk = K > 0 ? (K + splits - 1) / splits : 1;
-  kchunk = (kchunk + 15) / 16 * 16;
+  kchunk = (kchunk + 31) / 32 * 32;  // a multiple of both k-tiles
   // float4 operand tiles: aligned pointers, leading dimensions and contiguous
   // extents all multiples of 4 (so no vector straddles an edge)
   const bool vec = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (lda & 3) == 0 &&

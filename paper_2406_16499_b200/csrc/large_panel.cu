@@ -313,6 +313,19 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// element (r, q) of the panel view at base(r) + q * stride (QR: down a column
+// of M with stride ld; RQ: along a row of M, conjugated, stride -1)
+template <class T>
+__device__ __forceinline__ void view_row(const PanelArgs<T>& a, int r, T*& base, int64_t& stride) {
+  if (a.rq) {
+    base = a.M + a.r0 + (a.c0 - r) * a.ld;
+    stride = -1;
+  } else {
+    base = a.M + (a.r0 + r) + a.c0 * a.ld;
+    stride = a.ld;
+  }
+}
+
 template <int RPT, int NT>
 __global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelArgs<float> a) {
   constexpr int NW = NT / 32;
@@ -335,14 +348,22 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelArgs<float> a) {
   const int nb = a.nb;
   const int rb = rank * a.rc, re = min(a.L, rb + a.rc);
 
+  long long* pk0 = (a.probe && rank == 0 && tid == 0) ? a.probe + 8 * NB : nullptr;  // kernel-level stamps
+  if (pk0) pk0[0] = clock64();
   float P[RPT][NB];
   int row[RPT];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     row[i] = rb + tid + NT * i;
     const bool own = row[i] < re;
+    float* pb;
+    int64_t ps;
+    view_row(a, own ? row[i] : rb, pb, ps);  // running pointer: no per-load address arithmetic
 #pragma unroll
-    for (int k = 0; k < NB; ++k) P[i][k] = (own && k < nb) ? ld_view(a, row[i], k) : 0.f;
+    for (int k = 0; k < NB; ++k) {
+      P[i][k] = (own && k < nb) ? *pb : 0.f;
+      pb += ps;
+    }
     if (!own) row[i] = -1;  // never > q, never == q
   }
   for (int e = tid; e < NB * NB; e += NT) G[e] = 0.f;
@@ -355,6 +376,7 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelArgs<float> a) {
   }
   cluster_barrier();  // every exchange barrier initialised before any remote signal
   const uint32_t xbytes = uint32_t(ncl) * (NB * sizeof(float) + sizeof(double)) + NB * sizeof(float);
+  if (pk0) pk0[1] = clock64();
   // exchange buffers and barrier as offsets from xd (the same in every CTA)
   const uint32_t off_d = uint32_t(__cvta_generic_to_shared(&xd[0][rank][0])) - xd0;
   const uint32_t off_p = uint32_t(__cvta_generic_to_shared(&xp[0][0])) - xd0;
@@ -504,37 +526,26 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelArgs<float> a) {
     }
     if (pq) pq[7] = clock64();
   }
+  if (pk0) pk0[2] = clock64();
   __syncthreads();
-  // ---- write back the factored panel and the dense reflector block; frame
-  //      index f holds column (nb + f) mod NB after nb steps
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int r = row[i];
-    if (r < 0) continue;
-    const int64_t vi = a.rq ? (a.c0 - r - a.vbase) : r;
-#pragma unroll
-    for (int f = 0; f < NB; ++f) {
-      const int k = (nb + f) & (NB - 1);
-      if (k < nb) {
-        st_view(a, r, k, P[i][f]);
-        a.V[vi + k * a.ldv] = r < k ? 0.f : (r == k ? 1.f : P[i][f]);
-      }
-    }
-  }
+  if (pk0) pk0[3] = clock64();
+  // ---- T of the panel first (rank 0, warp 0), overlapping the other warps'
+  //      write-back; then every thread writes its rows back through running
+  //      pointers (frame index f holds column (nb + f) mod NB after nb steps)
   if (rank == 0) {
     if (tid < nb) a.tau[tid] = taus[tid];
     if (w == 0) {
       // T[q][q] = tau_q ; T[0:q, q] = -tau_q T[0:q, 0:q] G[0:q, q]; lane l owns row l
       float Tr[NB];
 #pragma unroll
-      for (int k = 0; k < NB; ++k) Tr[k] = 0.f;
+      for (int k2 = 0; k2 < NB; ++k2) Tr[k2] = 0.f;
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
         if (q < nb) {
           float t = 0.f;
 #pragma unroll
-          for (int k = 0; k < NB; ++k)
-            if (k < q) t = fmaf(Tr[k], G[k + NB * q], t);
+          for (int k2 = 0; k2 < NB; ++k2)
+            if (k2 < q) t = fmaf(Tr[k2], G[k2 + NB * q], t);
           const float tq = taus[q];
           Tr[q] = l < q ? -(tq * t) : (l == q ? tq : 0.f);
         }
@@ -545,6 +556,25 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelArgs<float> a) {
           if (q < nb) a.Tm[l + q * NB] = Tr[q];
     }
   }
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int r = row[i];
+    if (r < 0) continue;
+    const int64_t vi = a.rq ? (a.c0 - r - a.vbase) : r;
+    float* pb;
+    int64_t ps;
+    view_row(a, r, pb, ps);
+    float* pv = a.V + vi;
+#pragma unroll
+    for (int f = 0; f < NB; ++f) {
+      const int kc = (nb + f) & (NB - 1);
+      if (kc < nb) {
+        pb[kc * ps] = P[i][f];
+        pv[kc * a.ldv] = r < kc ? 0.f : (r == kc ? 1.f : P[i][f]);
+      }
+    }
+  }
+  if (pk0) pk0[4] = clock64();
   cluster_barrier();
 }
 

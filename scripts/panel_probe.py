@@ -11,13 +11,16 @@ dev = torch.device("cuda")
 for L in [int(x) for x in sys.argv[1:]] or [8192, 4096]:
     Mx = torch.randn(32, L, device=dev)
     V = torch.empty(32, L, device=dev); tau = torch.empty(32, device=dev); T = torch.empty(32, 32, device=dev)
-    pr = torch.zeros(32 * 8, dtype=torch.int64, device=dev)
+    pr = torch.zeros(32 * 8 + 8, dtype=torch.int64, device=dev)
     for _ in range(3):
         M2 = Mx.clone()
         assert lib.mlsb_panel_probe_f32(M2.data_ptr(), L, L, 32, tau.data_ptr(), V.data_ptr(), T.data_ptr(),
                                         pr.data_ptr(), torch.cuda.current_stream().cuda_stream) == 0
         torch.cuda.synchronize()
-    p = pr.cpu().numpy().reshape(32, 8).astype(np.int64)
+    allp = pr.cpu().numpy().astype(np.int64)
+    kp = allp[256:261]
+    print(f"L={L}: kernel stamps: load {kp[1]-kp[0]} cyc, steps {kp[2]-kp[1]} cyc, writeback {kp[3]-kp[2]} cyc, T {kp[4]-kp[3]} cyc")
+    p = allp[:256].reshape(32, 8)
     names = ["partials+reduce", "sync1", "push", "wait", "coef", "sync2", "apply"]
     d = np.diff(p, axis=1)
     step = p[1:, 0] - p[:-1, 0]

@@ -606,8 +606,14 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel_c(PanelArgs<cf> a) {
   for (int i = 0; i < RPT; ++i) {
     row[i] = rb + tid + NT * i;
     const bool own = row[i] < re;
+    cf* pb;
+    int64_t ps;
+    view_row(a, own ? row[i] : rb, pb, ps);
 #pragma unroll
-    for (int k = 0; k < NB; ++k) P[i][k] = (own && k < nb) ? ld_view(a, row[i], k) : zero<cf>();
+    for (int k = 0; k < NB; ++k) {
+      P[i][k] = (own && k < nb) ? (a.rq ? conj_(*pb) : *pb) : zero<cf>();
+      pb += ps;
+    }
     if (!own) row[i] = -1;  // never > q, never == q
   }
   for (int e = tid; e < NB * NB; e += NT) G[e] = zero<cf>();
@@ -771,36 +777,20 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel_c(PanelArgs<cf> a) {
     if (pq) pq[7] = clock64();
   }
   __syncthreads();
-  // ---- write back the factored panel and the dense reflector block; frame
-  //      index f holds column (nb + f) mod NB after nb steps
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int r = row[i];
-    if (r < 0) continue;
-    const int64_t vi = a.rq ? (a.c0 - r - a.vbase) : r;
-#pragma unroll
-    for (int f = 0; f < NB; ++f) {
-      const int k = (nb + f) & (NB - 1);
-      if (k < nb) {
-        st_view(a, r, k, P[i][f]);
-        a.V[vi + k * a.ldv] = r < k ? zero<cf>() : (r == k ? one<cf>() : P[i][f]);
-      }
-    }
-  }
+  // ---- T first (rank 0, warp 0), then the write-back through running pointers
   if (rank == 0) {
     if (tid < nb) a.tau[tid] = taus[tid];
     if (w == 0) {
-      // T[q][q] = tau_q ; T[0:q, q] = -tau_q T[0:q, 0:q] G[0:q, q]; lane l owns row l
       cf Tr[NB];
 #pragma unroll
-      for (int k = 0; k < NB; ++k) Tr[k] = zero<cf>();
+      for (int k2 = 0; k2 < NB; ++k2) Tr[k2] = zero<cf>();
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
         if (q < nb) {
           cf t = zero<cf>();
 #pragma unroll
-          for (int k = 0; k < NB; ++k)
-            if (k < q) mac(t, Tr[k], G[k + NB * q]);
+          for (int k2 = 0; k2 < NB; ++k2)
+            if (k2 < q) mac(t, Tr[k2], G[k2 + NB * q]);
           const cf tq = taus[q];
           Tr[q] = l < q ? -(tq * t) : (l == q ? tq : zero<cf>());
         }
@@ -809,6 +799,24 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel_c(PanelArgs<cf> a) {
 #pragma unroll
         for (int q = 0; q < NB; ++q)
           if (q < nb) a.Tm[l + q * NB] = Tr[q];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int r = row[i];
+    if (r < 0) continue;
+    const int64_t vi = a.rq ? (a.c0 - r - a.vbase) : r;
+    cf* pb;
+    int64_t ps;
+    view_row(a, r, pb, ps);
+    cf* pv = a.V + vi;
+#pragma unroll
+    for (int f = 0; f < NB; ++f) {
+      const int kc = (nb + f) & (NB - 1);
+      if (kc < nb) {
+        pb[kc * ps] = a.rq ? conj_(P[i][f]) : P[i][f];
+        pv[kc * a.ldv] = r < kc ? zero<cf>() : (r == kc ? one<cf>() : P[i][f]);
+      }
     }
   }
   cluster_barrier();

@@ -33,11 +33,10 @@ struct Tile {
 };
 
 template <class T, class TL, bool HA, bool HB>
-__global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, T alpha,
-                                                   const T* __restrict__ A, int64_t lda,
-                                                   const T* __restrict__ B, int64_t ldb, T beta,
-                                                   T* __restrict__ C, int64_t ldc, int kchunk,
-                                                   int64_t split_stride) {
+__device__ __forceinline__ void gemm_tile_body(int M, int N, int K, T alpha, const T* __restrict__ A, int64_t lda,
+                                               const T* __restrict__ B, int64_t ldb, T beta, T* __restrict__ C,
+                                               int64_t ldc, int kchunk, int64_t split_stride, int bx, int by,
+                                               int bz) {
   constexpr int BM = TL::BM, BN = TL::BN, BK = TL::BK, TM = TL::TM, TN = TL::TN, RT = TL::RT;
   constexpr int PAD = 4;
   constexpr int LA = BM * BK / 256, LB = BN * BK / 256;  // elements per thread per tile
@@ -45,10 +44,10 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, T alpha,
   __shared__ __align__(16) T Bs[2][BK][BN + PAD];
 
   const int tid = threadIdx.x, tr = tid % RT, tc = tid / RT;
-  const int i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
-  const int kbeg = blockIdx.z * kchunk;
+  const int i0 = bx * BM, j0 = by * BN;
+  const int kbeg = bz * kchunk;
   const int kend = min(K, kbeg + kchunk);
-  C += int64_t(blockIdx.z) * split_stride;
+  C += int64_t(bz) * split_stride;
 
   T ra[LA], rb[LB];
   auto load_tiles = [&](int k0) {
@@ -139,6 +138,21 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, T alpha,
       if (beta != zero<T>()) v = v + beta * old[a];
       cj[gi] = v;
     }
+  }
+}
+
+// persistent wrapper: CTAs walk the (gm, gn, gz) tiles with a stride, so the
+// grid can be capped (g_gemm_cta_cap) to leave SMs to the look-ahead stream
+template <class T, class TL, bool HA, bool HB>
+__global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, T alpha, const T* __restrict__ A,
+                                                   int64_t lda, const T* __restrict__ B, int64_t ldb, T beta,
+                                                   T* __restrict__ C, int64_t ldc, int kchunk, int64_t split_stride,
+                                                   int gm, int gn, int gz) {
+  const int ntiles = gm * gn * gz;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    gemm_tile_body<T, TL, HA, HB>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, split_stride, t % gm,
+                                  (t / gm) % gn, t / (gm * gn));
+    __syncthreads();
   }
 }
 
@@ -380,18 +394,23 @@ __global__ void splitk_reduce(int M, int N, int splits, const T* __restrict__ pa
   }
 }
 
+static thread_local int g_gemm_cta_cap = 0;  // cap on resident CTAs of the trailing GEMMs (0 = none)
+void set_gemm_cta_cap(int cap) { g_gemm_cta_cap = cap; }
+
 template <class T, class TL>
-static cudaError_t launch(bool ha, bool hb, dim3 grid, int M, int N, int K, T alpha, const T* A,
+static cudaError_t launch(bool ha, bool hb, dim3 tiles, int M, int N, int K, T alpha, const T* A,
                           int64_t lda, const T* B, int64_t ldb, T beta, T* C, int64_t ldc,
                           int kchunk, int64_t sstr, cudaStream_t st) {
+  const int gm = int(tiles.x), gn = int(tiles.y), gz = int(tiles.z), nt = gm * gn * gz;
+  const int grid = g_gemm_cta_cap > 0 ? std::min(nt, g_gemm_cta_cap) : nt;
   if (!ha && !hb)
-    gemm_kernel<T, TL, false, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+    gemm_kernel<T, TL, false, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, gm, gn, gz);
   else if (ha && !hb)
-    gemm_kernel<T, TL, true, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+    gemm_kernel<T, TL, true, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, gm, gn, gz);
   else if (!ha && hb)
-    gemm_kernel<T, TL, false, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+    gemm_kernel<T, TL, false, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, gm, gn, gz);
   else
-    gemm_kernel<T, TL, true, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr);
+    gemm_kernel<T, TL, true, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, gm, gn, gz);
   return cudaGetLastError();
 }
 
@@ -442,9 +461,6 @@ static cudaError_t gemm_tile(bool ha, bool hb, int M, int N, int K, T alpha, con
   return cudaGetLastError();
 }
 
-// cap on resident CTAs of the big trailing GEMMs (0 = no cap), see sgemm128
-static thread_local int g_gemm_cta_cap = 0;
-void set_gemm_cta_cap(int cap) { g_gemm_cta_cap = cap; }
 
 constexpr int GBK = 32;  // k-tile of the binary32 WY GEMM (MLSB_GEMM_BK16=1: 16)
 template <bool VEC, int BK>

@@ -888,22 +888,22 @@ cudaError_t panel_factor(T* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb
     }
   }
   if constexpr (std::is_same<T, cf>::value) {
-    // complex64: 128 threads x 2 rows per CTA while 16 CTAs hold the panel
-    if (L <= PCL * 128 * 2 && !smem_panel) {
+    // complex64: 256 threads x 1 row per CTA while 16 CTAs hold the panel
+    if (L <= PCL * 256 && !smem_panel) {
       const int ncl = std::min(PCL, (L + 255) / 256);
       a.ncl = ncl;
       a.rc = (L + ncl - 1) / ncl;
       static bool attr_c = false;
       if (!attr_c) {
-        if ((e = cudaFuncSetAttribute(panel_reg_kernel_c<2, 128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)))
+        if ((e = cudaFuncSetAttribute(panel_reg_kernel_c<1, 256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)))
           return e;
         attr_c = true;
       }
       cfg.gridDim = dim3(ncl);
-      cfg.blockDim = dim3(128);
+      cfg.blockDim = dim3(256);
       cfg.dynamicSmemBytes = 0;
       attr[0].val.clusterDim.x = ncl;
-      return cudaLaunchKernelEx(&cfg, panel_reg_kernel_c<2, 128>, a);
+      return cudaLaunchKernelEx(&cfg, panel_reg_kernel_c<1, 256>, a);
     }
   }
   const size_t sm = panel_smem<T>(a.rc);

@@ -33,6 +33,9 @@ int mlsb_wy_gemm_f32(int ta, int tb, int M, int N, int K, float alpha, const flo
                      size_t work_elems, void* stream);
 int mlsb_panel_f32(float* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb, float* tau, float* V,
                    int64_t ldv, float* T, void* stream);
+/* the complex64 panel (interleaved re, im; ld, ldv in complex elements) */
+int mlsb_panel_c64(float* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb, float* tau, float* V,
+                   int64_t ldv, float* T, void* stream);
 /* the same panel (r0 = c0 = 0, ldv = L) with clock64 stamps of CTA 0 /
  * thread 0 written to probe[8 q + phase] for each reflector q */
 int mlsb_panel_probe_f32(float* M, int64_t ld, int L, int nb, float* tau, float* V, float* T,

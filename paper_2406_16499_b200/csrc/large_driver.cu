@@ -381,7 +381,11 @@ struct Streams {
 // resident-CTA cap of a trailing update that runs beside a look-ahead block
 // factorization: 148 + 100 CTAs of the 2-per-SM GEMM tile leave one slot free
 // on 48 SMs for the panel cluster and the small inner-update GEMMs
-constexpr int kTrailCap = 148 + 100;
+static int trail_cap() {
+  static const int v = getenv("MLSB_TRAIL_CAP") ? atoi(getenv("MLSB_TRAIL_CAP")) : 148 + 100;
+  return v;
+}
+#define kTrailCap trail_cap()
 
 // C2 := P^H C2 = C2 - V T^H (V^H C2) for C2 = M[j0:j0+L, c0:c0+nc]
 template <class FT>

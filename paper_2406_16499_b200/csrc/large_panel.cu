@@ -937,6 +937,13 @@ extern "C" int mlsb_panel_f32(float* M, int64_t ld, int64_t r0, int64_t c0, int 
   return int(mlsb::lg::panel_factor<float>(M, ld, r0, c0, L, nb, false, tau, V, ldv, T, 0,
                                            static_cast<cudaStream_t>(stream)));
 }
+extern "C" int mlsb_panel_c64(float* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb, float* tau, float* V,
+                              int64_t ldv, float* T, void* stream) {
+  using mlsb::lg::cf;
+  return int(mlsb::lg::panel_factor<cf>(reinterpret_cast<cf*>(M), ld, r0, c0, L, nb, false,
+                                        reinterpret_cast<cf*>(tau), reinterpret_cast<cf*>(V), ldv,
+                                        reinterpret_cast<cf*>(T), 0, static_cast<cudaStream_t>(stream)));
+}
 extern "C" int mlsb_panel_probe_f32(float* M, int64_t ld, int L, int nb, float* tau, float* V, float* T,
                                     long long* probe, void* stream) {
   return int(mlsb::lg::panel_factor<float>(M, ld, 0, 0, L, nb, false, tau, V, L, T, 0,

@@ -81,3 +81,17 @@ out.append(dict(case=f"panel {L}x32", us=round(1e3 * min(ts), 1), us_per_reflect
                 rel_err_R=prel))
 for o in out:
     print(json.dumps(o))
+
+# complex64 panel (C5's QR panels have 4096 rows)
+lib.mlsb_panel_c64.argtypes = lib.mlsb_panel_f32.argtypes
+Lc = 4096
+Mc = torch.randn(32, Lc, 2, device=dev)
+Vc = torch.empty(32, Lc, 2, device=dev); tc_ = torch.empty(32, 2, device=dev); Tc = torch.empty(32, 32, 2, device=dev)
+ts = []
+for _ in range(10):
+    M2 = Mc.clone()
+    ev0.record()
+    assert lib.mlsb_panel_c64(M2.data_ptr(), Lc, 0, 0, Lc, 32, tc_.data_ptr(), Vc.data_ptr(), Lc, Tc.data_ptr(), st) == 0
+    ev1.record(); torch.cuda.synchronize()
+    ts.append(ev0.elapsed_time(ev1))
+print(json.dumps(dict(case=f"complex panel {Lc}x32", us=round(1e3 * min(ts), 1), us_per_reflector=round(1e3 * min(ts) / 32, 2))))

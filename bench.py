@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip the C3 large-path record")
     return ap.parse_args()
 
 
@@ -346,8 +347,71 @@ def run_ours(args, rank, world, local_rank):
         del An, Bn
     if not args.no_e2e:
         del hA, hB
+    # ---- the large-problem path on this GPU (BASELINE config 3, one solve) and
+    # its trailing-update GEMM at the C3 shape, for the record (rank 0, N = 1)
+    if rank == 0 and world == 1 and not args.no_large:
+        del A, B
+        torch.cuda.empty_cache()
+        result["large_path"] = large_path_record(peak32)
     if rank == 0:
         emit(result)
+
+
+def large_path_record(peak32):
+    """C3 (LSE 8192x4096/1024, kappa_A 1e4) through the public API, device phase
+    times from the trace, plus the binary32 WY GEMM C -= V W2 (8192 x 3968,
+    K = 128) timed with CUDA events."""
+    import numpy as np
+    import torch
+
+    import paper_2406_16499_b200 as PK
+    from paper_2406_16499_b200 import _capi
+    from paper_2406_16499_b200 import generate as G
+
+    c = G.CONFIGS["C3"]
+    t0 = time.perf_counter()
+    A3, B3, b3, d3 = G.lse_problem(c["m"], c["n"], c["p"], c["kappa_A"], c["kappa_B"], c["seed"])
+    gen_s = time.perf_counter() - t0
+    cfg3 = PK.RefinementConfig(maxit=c["maxit"])
+    PK.mplse(PK.LseProblem(A3, B3, b3, d3), cfg3)  # warm-up (allocator, module load)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = PK.mplse(PK.LseProblem(A3, B3, b3, d3), cfg3)
+    wall = time.perf_counter() - t0
+    ph = {k: float(v) for k, v in res.trace.timing.items()}
+    dev_s = sum(ph.values())
+    out = {"workload": "C3 LSE 8192x4096/1024, kappa_A 1e4, (s,s,d,d), one solve via mplse (host arrays)",
+           "status": res.trace.status, "iterations": res.trace.iterations,
+           "device_ms": dev_s * 1e3, "wall_ms_incl_host_staging": wall * 1e3,
+           "phases_ms": {k: v * 1e3 for k, v in ph.items()}, "input_generation_s": gen_s,
+           "grq_tflops": grq_flops(c["m"], c["n"], c["p"]) / ph["factorization"] / 1e12}
+    # the trailing-update GEMM at the C3 QR-stage shape
+    lib = _capi.lib
+    lib.mlsb_wy_gemm_f32.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_void_p,
+                                     C.c_int64, C.c_void_p, C.c_int64, C.c_float, C.c_void_p, C.c_int64,
+                                     C.c_void_p, C.c_size_t, C.c_void_p]
+    Mm, Nn, Kk = 8192, 3968, 128
+    dev = torch.device("cuda")
+    Va = torch.randn(Kk, Mm, device=dev)
+    Wb = torch.randn(Nn, Kk, device=dev)
+    Cc = torch.randn(Nn, Mm, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    call = lambda: lib.mlsb_wy_gemm_f32(0, 0, Mm, Nn, Kk, -1.0, Va.data_ptr(), Mm, Wb.data_ptr(), Kk, 1.0,  # noqa: E731
+                                        Cc.data_ptr(), Mm, None, 0, st)
+    for _ in range(3):
+        call()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(20):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 20
+    tf = 2.0 * Mm * Nn * Kk / ms / 1e9
+    out["trailing_update_gemm"] = {"shape": "C -= V W2, 8192 x 3968, K = 128 (binary32 SIMT FFMA)",
+                                   "ms": ms, "tflops": tf, "peak_tflops": peak32,
+                                   "frac": tf / peak32 if peak32 > 0 else None}
+    return out
 
 
 def run_single(args):

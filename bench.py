@@ -288,24 +288,29 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- e2e: the public C ABI with pinned host buffers ----------------------
     if not args.no_e2e:
-        hA = torch.empty_strided(A.shape, A.stride(), dtype=A.dtype, pin_memory=True)
-        hA.copy_(A)
-        hB = torch.empty_strided(B.shape, B.stride(), dtype=B.dtype, pin_memory=True)
-        hB.copy_(B)
-        hb = b.cpu().pin_memory()
-        hd = d.cpu().pin_memory()
-        ox = torch.empty((batch, N), dtype=torch.float64, pin_memory=True)
-        orr = torch.empty((batch, M), dtype=torch.float64, pin_memory=True)
-        ov = torch.empty((batch, P), dtype=torch.float64, pin_memory=True)
-        ost = torch.empty(batch, dtype=torch.int32, pin_memory=True)
-        oit = torch.empty(batch, dtype=torch.int64, pin_memory=True)
-        oerr = torch.empty(batch, dtype=torch.int32, pin_memory=True)
+        # with several ranks on one host the pinned copies are bounded (16,384
+        # problems = 4.9 GB per rank) so that 8 ranks fit in host memory
+        eb = batch if world == 1 else min(batch, 16384)
+        Ae, Be = A[:eb], B[:eb]
+        hA = torch.empty_strided(Ae.shape, Ae.stride(), dtype=A.dtype, pin_memory=True)
+        hA.copy_(Ae)
+        hB = torch.empty_strided(Be.shape, Be.stride(), dtype=B.dtype, pin_memory=True)
+        hB.copy_(Be)
+        del Ae, Be
+        hb = b[:eb].cpu().pin_memory()
+        hd = d[:eb].cpu().pin_memory()
+        ox = torch.empty((eb, N), dtype=torch.float64, pin_memory=True)
+        orr = torch.empty((eb, M), dtype=torch.float64, pin_memory=True)
+        ov = torch.empty((eb, P), dtype=torch.float64, pin_memory=True)
+        ost = torch.empty(eb, dtype=torch.int32, pin_memory=True)
+        oit = torch.empty(eb, dtype=torch.int64, pin_memory=True)
+        oerr = torch.empty(eb, dtype=torch.int32, pin_memory=True)
         ccfg = cfg.to_c()
         ex = _capi.Exec(_capi.MLSB_HOST, -1, C.c_void_p(stream.cuda_stream))
         vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
 
         def e2e_step():
-            rc = lib.mlsb_mplse_batched(batch, vp(hA), M, hA.stride(0), vp(hB), P, hB.stride(0),
+            rc = lib.mlsb_mplse_batched(eb, vp(hA), M, hA.stride(0), vp(hB), P, hB.stride(0),
                                         vp(hb), M, vp(hd), P, M, N, P, C.byref(ccfg), vp(ox),
                                         vp(orr), vp(ov), vp(ost), vp(oit), vp(oerr), None, None,
                                         C.byref(ex))
@@ -326,10 +331,11 @@ def run_ours(args, rank, world, local_rank):
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         dt = float(tt.item())
         h2d = (hA.numel() + hB.numel() + hb.numel() + hd.numel()) * 8
-        d2h = (ox.numel() + orr.numel() + ov.numel()) * 8 + batch * (4 + 8 + 4)
-        result["e2e"] = {"value": world * batch * ke / dt, "unit": "solves/s",
+        d2h = (ox.numel() + orr.numel() + ov.numel()) * 8 + eb * (4 + 8 + 4)
+        result["e2e"] = {"value": world * eb * ke / dt, "unit": "solves/s",
                          "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                         "steps": ke, "api": "mlsb_mplse_batched (C ABI), pinned host buffers"}
+                         "steps": ke, "problems_per_rank": eb,
+                         "api": "mlsb_mplse_batched (C ABI), pinned host buffers"}
 
     # ---- CPU baseline: the reference on this host, bounded sample, rank 0, N=1
     # (the full batch when it fits in ~cpu_seconds)

@@ -7,6 +7,7 @@
 //
 //   auto res = mixedls::b200::mplse(pb, cfg);   // instead of mixedls::mplse(pb, cfg)
 //   auto res = mixedls::b200::mpgls(pb, cfg);   // instead of mixedls::mpgls(pb, cfg)
+//   (with MIXEDLS_B200_KRYLOV and <mixedls/krylov.hpp>: gmres_refine_lse / _gls too)
 //
 // Same argument and result types (lse_problem / gls_problem /
 // refinement_config -> mplse_result / mpgls_result, inc/lse.hpp:294-303,
@@ -151,6 +152,64 @@ inline gls_state gls_direct_reference(const gls_problem& pb) {
   detail::throw_for(rc, sing);
   return st;
 }
+
+#ifdef MIXEDLS_B200_KRYLOV
+// GPU drop-ins for mixedls::gmres_refine_lse / gmres_refine_gls
+// (inc/krylov.hpp:545, :673).  Define MIXEDLS_B200_KRYLOV and include
+// <mixedls/krylov.hpp> before this header.
+inline mplse_result gmres_refine_lse(const lse_problem& pb, const refinement_config& cfg,
+                                     precond_choice choice = precond_choice::bd_split,
+                                     double alpha_scale = 1.0) {
+  pb.validate();
+  cfg.validate();
+  const auto m = static_cast<int64_t>(pb.m()), n = static_cast<int64_t>(pb.n()),
+             p = static_cast<int64_t>(pb.p());
+  mplse_result out;
+  out.state.x.assign(n, 0.0);
+  out.state.r.assign(m, 0.0);
+  out.state.v.assign(p, 0.0);
+  std::vector<double> hist(3 * cfg.maxit);
+  mlsb_trace tr{};
+  tr.residual_history = hist.data();
+  int64_t sing = -1;
+  const mlsb_config c = detail::to_c(cfg);
+  const int rc = mlsb_gmres_lse(pb.A.data().data(), m, pb.B.data().data(), p, pb.b.data(), pb.d.data(),
+                                m, n, p, &c,
+                                choice == precond_choice::left ? MLSB_PRECOND_LEFT : MLSB_PRECOND_BD_SPLIT,
+                                alpha_scale, out.state.x.data(), out.state.r.data(), out.state.v.data(), &tr,
+                                &sing, nullptr);
+  detail::throw_for(rc, sing);
+  detail::fill_trace(out.trace, tr, hist);
+  out.trace.inner_iterations = static_cast<std::size_t>(tr.inner_iterations);
+  return out;
+}
+
+inline mpgls_result gmres_refine_gls(const gls_problem& pb, const refinement_config& cfg,
+                                     precond_choice choice = precond_choice::bd_split,
+                                     double alpha_scale = 1.0) {
+  pb.validate();
+  cfg.validate();
+  const auto n = static_cast<int64_t>(pb.n()), m = static_cast<int64_t>(pb.m()),
+             p = static_cast<int64_t>(pb.p());
+  mpgls_result out;
+  out.state.x.assign(m, 0.0);
+  out.state.y.assign(p, 0.0);
+  out.state.z.assign(n, 0.0);
+  std::vector<double> hist(3 * cfg.maxit);
+  mlsb_trace tr{};
+  tr.residual_history = hist.data();
+  int64_t sing = -1;
+  const mlsb_config c = detail::to_c(cfg);
+  const int rc = mlsb_gmres_gls(pb.W.data().data(), n, pb.V.data().data(), n, pb.d.data(), n, m, p, &c,
+                                choice == precond_choice::left ? MLSB_PRECOND_LEFT : MLSB_PRECOND_BD_SPLIT,
+                                alpha_scale, out.state.x.data(), out.state.y.data(), out.state.z.data(), &tr,
+                                &sing, nullptr);
+  detail::throw_for(rc, sing);
+  detail::fill_trace(out.trace, tr, hist);
+  out.trace.inner_iterations = static_cast<std::size_t>(tr.inner_iterations);
+  return out;
+}
+#endif  // MIXEDLS_B200_KRYLOV
 
 }  // namespace b200
 }  // namespace mixedls

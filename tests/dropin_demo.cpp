@@ -8,7 +8,9 @@
 #include "mixedls/experiment.hpp"
 #include "mixedls/generate.hpp"
 #include "mixedls/gls.hpp"
+#include "mixedls/krylov.hpp"
 #include "mixedls/lse.hpp"
+#define MIXEDLS_B200_KRYLOV
 #include "mixedls_b200.hpp"
 
 using namespace mixedls;
@@ -55,6 +57,19 @@ int main() {
   auto dref = detail::lse_direct_reference(pb).state;
   auto dgpu = b200::lse_direct_reference(pb);
   std::printf("DIRECT relx %.3e relr %.3e\n", reldiff(dgpu.x, dref.x), reldiff(dgpu.r, dref.r));
+  // GMRES-IR drop-ins (krylov.hpp:545, :673), both preconditioners
+  for (precond_choice pc : {precond_choice::bd_split, precond_choice::left}) {
+    auto rg = gmres_refine_lse(pb, cfg, pc);
+    auto gg2 = b200::gmres_refine_lse(pb, cfg, pc);
+    std::printf("GMRES-LSE %d ref_iters %zu gpu_iters %zu ref_status %s gpu_status %s relx %.3e\n", int(pc),
+                rg.trace.iterations, gg2.trace.iterations, to_string(rg.trace.status),
+                to_string(gg2.trace.status), reldiff(gg2.state.x, rg.state.x));
+    auto rgl = gmres_refine_gls(pg, cfg, pc);
+    auto ggl = b200::gmres_refine_gls(pg, cfg, pc);
+    std::printf("GMRES-GLS %d ref_iters %zu gpu_iters %zu ref_status %s gpu_status %s relx %.3e\n", int(pc),
+                rgl.trace.iterations, ggl.trace.iterations, to_string(rgl.trace.status),
+                to_string(ggl.trace.status), reldiff(ggl.state.x, rgl.state.x));
+  }
   // exception parity: the reference's validation is reused verbatim
   lse_problem bad = pb;
   bad.d.pop_back();

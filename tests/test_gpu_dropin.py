@@ -26,6 +26,11 @@ def test_reference_program_through_shim(gpu):
     assert "EXC dimension_error" in out
     dr = re.search(r"DIRECT relx (\S+) relr (\S+)", out)
     assert dr and float(dr[1]) <= 1e-9 and float(dr[2]) <= 1e-9, out
+    gm = re.findall(r"GMRES-(LSE|GLS) (\d) ref_iters (\d+) gpu_iters (\d+) ref_status (\w+) gpu_status (\w+) relx (\S+)", out)
+    assert len(gm) == 4, out
+    for kind, _, ri, gi, rs, gs, rx in gm:
+        assert rs == gs == "converged" and abs(int(ri) - int(gi)) <= 1, (kind, ri, gi, rs, gs)
+        assert float(rx) <= 1e-9, (kind, rx)
 
 
 def test_dropin_demo_exception_path_without_gpu():

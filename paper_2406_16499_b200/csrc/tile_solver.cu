@@ -249,12 +249,27 @@ __device__ void gen_col_reflector(FT* col, int j, int rend, FT* tau_j, int lane)
 // One reflector per step; column c is owned by warp c % NW, and the owner of
 // column j+1 generates reflector j+1 right after applying H_j to it
 // (look-ahead), so each step costs one CTA barrier.
+//
+// Reflector j is published through a ring of mbarriers (one arrival: the
+// owner warp's lane 0 after a __syncwarp) instead of a CTA barrier per step:
+// a warp waits only for the reflector it applies next, so the owner of column
+// j+1 never waits for the slowest warp's bulk updates.  Every warp owns a
+// column every NW steps, so no warp lags more than NW steps: a ring of 2 NW
+// barriers cannot wrap onto a pending phase.
 template <class FT>
 __device__ void qr_stage(FT* M, int ld, int rend, int k, int cend, FT* tau, int warp, int lane) {
   if (k <= 0) return;
-  if (warp == 0) gen_col_reflector(M, 0, rend, &tau[0], lane);
+  constexpr int NQB = 2 * NW;
+  __shared__ uint64_t qbar[NQB];
+  if (warp == 0 && lane < NQB) mbar_init(&qbar[lane], 1);
+  __syncthreads();
+  if (warp == 0) {
+    gen_col_reflector(M, 0, rend, &tau[0], lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&qbar[0]);
+  }
   for (int j = 0; j < k; ++j) {
-    __syncthreads();
+    mbar_wait(&qbar[j % NQB], (j / NQB) & 1);
     const FT tj = tau[j];
     const FT* v = M + size_t(j) * ld;
     int c = j + 1 + ((warp - (j + 1)) % NW + NW) % NW;
@@ -271,7 +286,11 @@ __device__ void qr_stage(FT* M, int ld, int rend, int k, int cend, FT* tau, int 
         if (lane == 0) cc[j] -= s;
         for (int i = j + 1 + lane; i < rend; i += 32) cc[i] -= s * v[i];
       }
-      if (c < k) gen_col_reflector(cc, c, rend, &tau[c], lane);
+      if (c < k) {
+        gen_col_reflector(cc, c, rend, &tau[c], lane);
+        __syncwarp();  // the warp's writes of v_{j+1} and tau before lane 0's release
+        if (lane == 0) mbar_arrive(&qbar[c % NQB]);
+      }
       c += NW;
     }
     if (tj != FT(0)) {
@@ -280,6 +299,7 @@ __device__ void qr_stage(FT* M, int ld, int rend, int k, int cend, FT* tau, int 
         FT* cc[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) cc[u] = M + size_t(min(c + u * NW, cend - 1)) * ld;
+#pragma unroll 4
         for (int i = j + 1 + lane; i < rend; i += 32) {
           const FT vi = v[i];
 #pragma unroll
@@ -292,12 +312,22 @@ __device__ void qr_stage(FT* M, int ld, int rend, int k, int cend, FT* tau, int 
           cj[u] = cc[u][j];
         }
         __syncwarp();  // every lane has read cc[u][j] before lane 0 rewrites it
+        FT su[4];
+        bool live[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          if (c + u * NW >= cend) break;
-          const FT su = (s[u] + cj[u]) * tj;
-          if (lane == 0) cc[u][j] = cj[u] - su;
-          for (int i = j + 1 + lane; i < rend; i += 32) cc[u][i] -= su * v[i];
+          live[u] = c + u * NW < cend;
+          su[u] = (s[u] + cj[u]) * tj;
+          if (lane == 0 && live[u]) cc[u][j] = cj[u] - su[u];
+        }
+        // one pass over the rows for the four columns: v[i] read once, the
+        // column loads independent of each other (no per-column latency chain)
+#pragma unroll 4
+        for (int i = j + 1 + lane; i < rend; i += 32) {
+          const FT vi = v[i];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (live[u]) cc[u][i] -= su[u] * vi;
         }
       }
     }
@@ -418,6 +448,7 @@ __global__ void __launch_bounds__(NT, 1) tile_solve_kernel(TileArgs a) {
     }
   };
   if (tid == 0) t_last = globaltimer_ns();
+  if (a.stamps && pid == 0 && tid == 0) a.stamps[0] = t_last;  // debug: kernel start
   if (tid == 0) {
     iflag[0] = 0;
     iflag[1] = -1;
@@ -527,6 +558,7 @@ __global__ void __launch_bounds__(NT, 1) tile_solve_kernel(TileArgs a) {
   }
   __syncthreads();
   lap(5);
+  if (a.stamps && pid == 0 && tid == 0) a.stamps[29] = globaltimer_ns();  // debug: factorization start
 
   // ---------------- GRQ / GQR at u_f ------------------------------------------
   if (KIND == KIND_LSE) {
@@ -534,7 +566,9 @@ __global__ void __launch_bounds__(NT, 1) tile_solve_kernel(TileArgs a) {
     qr_stage<FT>(M, ld, m, m < n ? m : n, n, tau1, warp, lane);
   } else {
     qr_stage<FT>(M, ld, n, m, m + p, tau1, warp, lane);
+    if (a.stamps && pid == 0 && tid == 0) a.stamps[30] = globaltimer_ns();  // debug: QR stage done
     rq_stage<FT>(M, ld, 0, n, m, p, tau2, scal, tid, warp, lane);
+    if (a.stamps && pid == 0 && tid == 0) a.stamps[31] = globaltimer_ns();  // debug: RQ stage done
   }
   __syncthreads();
   lap(0);

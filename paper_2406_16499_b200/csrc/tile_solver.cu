@@ -382,12 +382,15 @@ __device__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, int cc, FT* tau,
         FT* arow = M + (ok ? i : 0) + size_t(c0) * ld;
         FT w = FT(0);
         const FT apc = ok ? arow[size_t(pc) * ld] : FT(0);
-        if (ok)
+        if (ok) {
+#pragma unroll 4
           for (int q = qa; q < qb; ++q) w += vrow[size_t(q) * ld] * arow[size_t(q) * ld];
+        }
         w += __shfl_xor_sync(0xffffffffu, w, 1);
         w += __shfl_xor_sync(0xffffffffu, w, 2);
         w += apc;
         if (ok) {
+#pragma unroll 4
           for (int q = qa; q < qb; ++q) arow[size_t(q) * ld] -= (tj * vrow[size_t(q) * ld]) * w;
           if (c == 0) arow[size_t(pc) * ld] = apc - tj * w;
         }

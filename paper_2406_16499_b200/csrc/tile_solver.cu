@@ -46,6 +46,7 @@ constexpr int NW = NT / 32;
 constexpr int RPL = 2;         // rows per lane in a residual chunk
 constexpr int CH = 32 * RPL;   // rows per residual chunk
 constexpr int NWORK = 8;       // solve-precision work vectors
+constexpr size_t kStaticSmem = 512;  // qr_stage's static mbarrier ring, counted against the limit
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -1152,7 +1153,7 @@ size_t tile_smem_bytes(int kind, int64_t m, int64_t n, int64_t p, int u_f, int u
                        bool m_global) {
   const int fsz = u_f == 0 ? 4 : 8, csz = u_s == 0 ? 4 : 8;
   const Layout L = make_layout(kind, m, n, p, fsz, csz, u_r == 2, m_global);
-  return L.total;
+  return L.total + kStaticSmem;
 }
 
 size_t tile_gws_bytes(int kind, int64_t m, int64_t n, int64_t p, int u_f) {

@@ -258,7 +258,7 @@ __device__ void gen_col_reflector(FT* col, int j, int rend, FT* tau_j, int lane)
 // column every NW steps, so no warp lags more than NW steps: a ring of 2 NW
 // barriers cannot wrap onto a pending phase.
 template <class FT>
-__device__ void qr_stage(FT* M, int ld, int rend, int k, int cend, FT* tau, int warp, int lane) {
+__device__ __forceinline__ void qr_stage(FT* M, int ld, int rend, int k, int cend, FT* tau, int warp, int lane) {
   if (k <= 0) return;
   constexpr int NQB = 2 * NW;
   __shared__ uint64_t qbar[NQB];
@@ -340,7 +340,7 @@ __device__ void qr_stage(FT* M, int ld, int rend, int k, int cend, FT* tau, int 
 // generated from row rb+rr-kk+j and applied from the right to every row
 // above it.  The reference's sequential row-dot order is kept per thread.
 template <class FT>
-__device__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, int cc, FT* tau, double* scal,
+__device__ __forceinline__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, int cc, FT* tau, double* scal,
                          int tid, int warp, int lane) {
   const int kk = rr < cc ? rr : cc;
   for (int j = kk - 1; j >= 0; --j) {
@@ -374,26 +374,72 @@ __device__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, int cc, FT* tau,
     if (tj != FT(0)) {
       // 4 threads per row (adjacent lanes), each with a quarter of the row's
       // dot: chains of ~pc/4 FMAs instead of pc, every thread of the CTA busy;
-      // the quarters are combined as (q0 + q1) + (q2 + q3) (same in every lane)
+      // the quarters are combined as (q0 + q1) + (q2 + q3) (same in every
+      // lane).  Two rows (i, i + NT/4) per thread when both passes are live,
+      // so each v element is loaded once for both.
       const int qc = (pc + 3) / 4, c = lane & 3, r8 = lane >> 2;
       const int qa = min(pc, c * qc), qb = min(pc, qa + qc);
-      for (int i0 = 0; i0 < row; i0 += NT / 4) {
+      const FT* vq = vrow + size_t(qa) * ld;
+      FT* Mc = M + size_t(c0) * ld;  // column block of this stage
+      for (int i0 = 0; i0 + warp * 8 < row; i0 += NT / 2) {
         const int i = i0 + warp * 8 + r8;
         const bool ok = i < row;
-        FT* arow = M + (ok ? i : 0) + size_t(c0) * ld;
-        FT w = FT(0);
-        const FT apc = ok ? arow[size_t(pc) * ld] : FT(0);
-        if (ok) {
+        if (i0 + NT / 4 + warp * 8 < row) {  // warp-uniform: second pass live
+          const bool ok2 = i + NT / 4 < row;
+          FT* a1 = Mc + i + size_t(qa) * ld;
+          FT* a2 = Mc + (ok2 ? i + NT / 4 : i) + size_t(qa) * ld;
+          const FT apc1 = Mc[i + size_t(pc) * ld];
+          const FT apc2 = ok2 ? Mc[i + NT / 4 + size_t(pc) * ld] : FT(0);
+          FT w1 = FT(0), w2 = FT(0);
+          {
+            const FT *v = vq, *p1 = a1, *p2 = a2;
 #pragma unroll 4
-          for (int q = qa; q < qb; ++q) w += vrow[size_t(q) * ld] * arow[size_t(q) * ld];
-        }
-        w += __shfl_xor_sync(0xffffffffu, w, 1);
-        w += __shfl_xor_sync(0xffffffffu, w, 2);
-        w += apc;
-        if (ok) {
+            for (int q = qa; q < qb; ++q, v += ld, p1 += ld, p2 += ld) {
+              const FT vv = *v;
+              w1 += vv * *p1;
+              w2 += vv * *p2;
+            }
+          }
+          w1 += __shfl_xor_sync(0xffffffffu, w1, 1);
+          w2 += __shfl_xor_sync(0xffffffffu, w2, 1);
+          w1 += __shfl_xor_sync(0xffffffffu, w1, 2);
+          w2 += __shfl_xor_sync(0xffffffffu, w2, 2);
+          w1 += apc1;
+          w2 += apc2;
+          {
+            const FT* v = vq;
+            FT *p1 = a1, *p2 = a2;
 #pragma unroll 4
-          for (int q = qa; q < qb; ++q) arow[size_t(q) * ld] -= (tj * vrow[size_t(q) * ld]) * w;
-          if (c == 0) arow[size_t(pc) * ld] = apc - tj * w;
+            for (int q = qa; q < qb; ++q, v += ld, p1 += ld, p2 += ld) {
+              const FT tv = tj * *v;
+              *p1 -= tv * w1;
+              if (ok2) *p2 -= tv * w2;
+            }
+          }
+          if (c == 0) {
+            Mc[i + size_t(pc) * ld] = apc1 - tj * w1;
+            if (ok2) Mc[i + NT / 4 + size_t(pc) * ld] = apc2 - tj * w2;
+          }
+        } else {
+          FT* arow = Mc + (ok ? i : 0);
+          FT w = FT(0);
+          const FT apc = ok ? arow[size_t(pc) * ld] : FT(0);
+          if (ok) {
+            const FT* v = vq;
+            const FT* p1 = arow + size_t(qa) * ld;
+#pragma unroll 4
+            for (int q = qa; q < qb; ++q, v += ld, p1 += ld) w += *v * *p1;
+          }
+          w += __shfl_xor_sync(0xffffffffu, w, 1);
+          w += __shfl_xor_sync(0xffffffffu, w, 2);
+          w += apc;
+          if (ok) {
+            const FT* v = vq;
+            FT* p1 = arow + size_t(qa) * ld;
+#pragma unroll 4
+            for (int q = qa; q < qb; ++q, v += ld, p1 += ld) *p1 -= (tj * *v) * w;
+            if (c == 0) arow[size_t(pc) * ld] = apc - tj * w;
+          }
         }
       }
     }
@@ -566,12 +612,16 @@ __global__ void __launch_bounds__(NT, 1) tile_solve_kernel(TileArgs a) {
 
   // ---------------- GRQ / GQR at u_f ------------------------------------------
   if (KIND == KIND_LSE) {
-    rq_stage<FT>(M, ld, m, p, 0, n, tau2, scal, tid, warp, lane);
-    qr_stage<FT>(M, ld, m, m < n ? m : n, n, tau1, warp, lane);
+    if (a.gws) rq_stage<FT>(M, ld, m, p, 0, n, tau2, scal, tid, warp, lane);
+    else rq_stage<FT>(reinterpret_cast<FT*>(smem + Ly.oM), ld, m, p, 0, n, tau2, scal, tid, warp, lane);
+    if (a.gws) qr_stage<FT>(M, ld, m, m < n ? m : n, n, tau1, warp, lane);
+    else qr_stage<FT>(reinterpret_cast<FT*>(smem + Ly.oM), ld, m, m < n ? m : n, n, tau1, warp, lane);
   } else {
-    qr_stage<FT>(M, ld, n, m, m + p, tau1, warp, lane);
+    if (a.gws) qr_stage<FT>(M, ld, n, m, m + p, tau1, warp, lane);
+    else qr_stage<FT>(reinterpret_cast<FT*>(smem + Ly.oM), ld, n, m, m + p, tau1, warp, lane);
     if (a.stamps && pid == 0 && tid == 0) a.stamps[30] = globaltimer_ns();  // debug: QR stage done
-    rq_stage<FT>(M, ld, 0, n, m, p, tau2, scal, tid, warp, lane);
+    if (a.gws) rq_stage<FT>(M, ld, 0, n, m, p, tau2, scal, tid, warp, lane);
+    else rq_stage<FT>(reinterpret_cast<FT*>(smem + Ly.oM), ld, 0, n, m, p, tau2, scal, tid, warp, lane);
     if (a.stamps && pid == 0 && tid == 0) a.stamps[31] = globaltimer_ns();  // debug: RQ stage done
   }
   __syncthreads();

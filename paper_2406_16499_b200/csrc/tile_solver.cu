@@ -449,21 +449,24 @@ __device__ __forceinline__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, 
 }
 
 // ============================== kernel =====================================
-template <int KIND, class FT, class CT, bool EXT>
+// MG: factors in the global workspace (a.gws) instead of shared memory; a
+// template parameter so that the shared-memory instantiation addresses M
+// with LDS/STS instead of generic loads.
+template <int KIND, class FT, class CT, bool EXT, bool MG>
 __global__ void __launch_bounds__(NT, 1) tile_solve_kernel(TileArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t pid = blockIdx.x;
   const int m = int(a.m), n = int(a.n), p = int(a.p);
-  const Layout Ly = make_layout(KIND, m, n, p, sizeof(FT), sizeof(CT), EXT, a.gws != nullptr);
+  const Layout Ly = make_layout(KIND, m, n, p, sizeof(FT), sizeof(CT), EXT, MG);
   const int R = Ly.R, C = Ly.C, ld = Ly.ld;
   constexpr bool LOWF = sizeof(FT) == 4;
   constexpr bool LOWS = sizeof(CT) == 4;
 
   // the stacked factor matrix lives in shared memory, or -- when it does not
   // fit -- in a per-problem global workspace that stays L2-resident
-  FT* M = a.gws ? reinterpret_cast<FT*>(a.gws) + size_t(pid) * size_t(ld) * C
-                : reinterpret_cast<FT*>(smem + Ly.oM);
+  FT* M = MG ? reinterpret_cast<FT*>(a.gws) + size_t(pid) * size_t(ld) * C
+             : reinterpret_cast<FT*>(smem + Ly.oM);
   FT* tau1 = reinterpret_cast<FT*>(smem + Ly.oTau1);
   FT* tau2 = reinterpret_cast<FT*>(smem + Ly.oTau2);
   double* rinit = reinterpret_cast<double*>(smem + Ly.oRinit);
@@ -612,16 +615,12 @@ __global__ void __launch_bounds__(NT, 1) tile_solve_kernel(TileArgs a) {
 
   // ---------------- GRQ / GQR at u_f ------------------------------------------
   if (KIND == KIND_LSE) {
-    if (a.gws) rq_stage<FT>(M, ld, m, p, 0, n, tau2, scal, tid, warp, lane);
-    else rq_stage<FT>(reinterpret_cast<FT*>(smem + Ly.oM), ld, m, p, 0, n, tau2, scal, tid, warp, lane);
-    if (a.gws) qr_stage<FT>(M, ld, m, m < n ? m : n, n, tau1, warp, lane);
-    else qr_stage<FT>(reinterpret_cast<FT*>(smem + Ly.oM), ld, m, m < n ? m : n, n, tau1, warp, lane);
+    rq_stage<FT>(M, ld, m, p, 0, n, tau2, scal, tid, warp, lane);
+    qr_stage<FT>(M, ld, m, m < n ? m : n, n, tau1, warp, lane);
   } else {
-    if (a.gws) qr_stage<FT>(M, ld, n, m, m + p, tau1, warp, lane);
-    else qr_stage<FT>(reinterpret_cast<FT*>(smem + Ly.oM), ld, n, m, m + p, tau1, warp, lane);
+    qr_stage<FT>(M, ld, n, m, m + p, tau1, warp, lane);
     if (a.stamps && pid == 0 && tid == 0) a.stamps[30] = globaltimer_ns();  // debug: QR stage done
-    if (a.gws) rq_stage<FT>(M, ld, 0, n, m, p, tau2, scal, tid, warp, lane);
-    else rq_stage<FT>(reinterpret_cast<FT*>(smem + Ly.oM), ld, 0, n, m, p, tau2, scal, tid, warp, lane);
+    rq_stage<FT>(M, ld, 0, n, m, p, tau2, scal, tid, warp, lane);
     if (a.stamps && pid == 0 && tid == 0) a.stamps[31] = globaltimer_ns();  // debug: RQ stage done
   }
   __syncthreads();
@@ -1170,15 +1169,20 @@ finish:
 }
 
 // ============================== host side ===================================
-template <int KIND, class FT, class CT, bool EXT>
-static cudaError_t launch_one(const TileArgs& a, cudaStream_t st) {
+template <int KIND, class FT, class CT, bool EXT, bool MG>
+static cudaError_t launch_mg(const TileArgs& a, cudaStream_t st) {
   const Layout L = make_layout(KIND, a.m, a.n, a.p, sizeof(FT), sizeof(CT), EXT, a.gws != nullptr);
-  auto kern = tile_solve_kernel<KIND, FT, CT, EXT>;
+  auto kern = tile_solve_kernel<KIND, FT, CT, EXT, MG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(L.total));
   if (e != cudaSuccess) return e;
   kern<<<dim3(unsigned(a.batch)), dim3(NT), L.total, st>>>(a);
   return cudaGetLastError();
+}
+
+template <int KIND, class FT, class CT, bool EXT>
+static cudaError_t launch_one(const TileArgs& a, cudaStream_t st) {
+  return a.gws ? launch_mg<KIND, FT, CT, EXT, true>(a, st) : launch_mg<KIND, FT, CT, EXT, false>(a, st);
 }
 
 template <int KIND>

@@ -372,19 +372,24 @@ __device__ __forceinline__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, 
     __syncthreads();
     const FT tj = tau[j];
     if (tj != FT(0)) {
-      // 4 threads per row (adjacent lanes), each with a quarter of the row's
-      // dot: chains of ~pc/4 FMAs instead of pc, every thread of the CTA busy;
-      // the quarters are combined as (q0 + q1) + (q2 + q3) (same in every
-      // lane).  Two rows (i, i + NT/4) per thread when both passes are live,
+      // 4 threads per row (adjacent lanes), each with every fourth column of
+      // the row's dot: chains of ~pc/4 FMAs instead of pc, every thread of
+      // the CTA busy; the phases are combined as (p0 + p1) + (p2 + p3) (same
+      // in every lane).  Two rows (i, i + NT/4) per thread when both passes are live,
       // so each v element is loaded once for both.
-      const int qc = (pc + 3) / 4, c = lane & 3, r8 = lane >> 2;
-      const int qa = min(pc, c * qc), qb = min(pc, qa + qc);
+      // Thread (r8, c) of a warp takes row wrow + 4 r8 and columns c, c+4, ...:
+      // banks (4 r8 + c ld) mod 32 are distinct for any odd ld, so the
+      // 8 rows x 4 column phases of a warp access are conflict-free.
+      const int c = lane & 3, r8 = lane >> 2;
+      const int qa = min(pc, c), qb = pc;
+      const size_t st = size_t(4) * ld;
+      const int wrow = 32 * (warp >> 2) + (warp & 3);
       const FT* vq = vrow + size_t(qa) * ld;
       FT* Mc = M + size_t(c0) * ld;  // column block of this stage
-      for (int i0 = 0; i0 + warp * 8 < row; i0 += NT / 2) {
-        const int i = i0 + warp * 8 + r8;
+      for (int i0 = 0; i0 + wrow < row; i0 += NT / 2) {
+        const int i = i0 + wrow + 4 * r8;
         const bool ok = i < row;
-        if (i0 + NT / 4 + warp * 8 < row) {  // warp-uniform: second pass live
+        if (i0 + NT / 4 + wrow < row) {  // warp-uniform: second pass live
           const bool ok2 = i + NT / 4 < row;
           FT* a1 = Mc + i + size_t(qa) * ld;
           FT* a2 = Mc + (ok2 ? i + NT / 4 : i) + size_t(qa) * ld;
@@ -394,7 +399,7 @@ __device__ __forceinline__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, 
           {
             const FT *v = vq, *p1 = a1, *p2 = a2;
 #pragma unroll 4
-            for (int q = qa; q < qb; ++q, v += ld, p1 += ld, p2 += ld) {
+            for (int q = qa; q < qb; q += 4, v += st, p1 += st, p2 += st) {
               const FT vv = *v;
               w1 += vv * *p1;
               w2 += vv * *p2;
@@ -410,7 +415,7 @@ __device__ __forceinline__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, 
             const FT* v = vq;
             FT *p1 = a1, *p2 = a2;
 #pragma unroll 4
-            for (int q = qa; q < qb; ++q, v += ld, p1 += ld, p2 += ld) {
+            for (int q = qa; q < qb; q += 4, v += st, p1 += st, p2 += st) {
               const FT tv = tj * *v;
               *p1 -= tv * w1;
               if (ok2) *p2 -= tv * w2;
@@ -428,7 +433,7 @@ __device__ __forceinline__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, 
             const FT* v = vq;
             const FT* p1 = arow + size_t(qa) * ld;
 #pragma unroll 4
-            for (int q = qa; q < qb; ++q, v += ld, p1 += ld) w += *v * *p1;
+            for (int q = qa; q < qb; q += 4, v += st, p1 += st) w += *v * *p1;
           }
           w += __shfl_xor_sync(0xffffffffu, w, 1);
           w += __shfl_xor_sync(0xffffffffu, w, 2);
@@ -437,7 +442,7 @@ __device__ __forceinline__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, 
             const FT* v = vq;
             FT* p1 = arow + size_t(qa) * ld;
 #pragma unroll 4
-            for (int q = qa; q < qb; ++q, v += ld, p1 += ld) *p1 -= (tj * *v) * w;
+            for (int q = qa; q < qb; q += 4, v += st, p1 += st) *p1 -= (tj * *v) * w;
             if (c == 0) arow[size_t(pc) * ld] = apc - tj * w;
           }
         }

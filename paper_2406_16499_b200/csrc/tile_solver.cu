@@ -246,6 +246,26 @@ __device__ void gen_col_reflector(FT* col, int j, int rend, FT* tau_j, int lane)
   __syncwarp();
 }
 
+// Four warp sums at once, bitwise equal to four warp_sum() butterflies (same
+// pairs at every level) in 10 shuffles instead of 20: the first two levels
+// halve the number of live values per lane (transposed reduction), the last
+// three are a plain butterfly, and the totals are broadcast back.
+template <class FT>
+__device__ __forceinline__ void warp_sum4(FT s[4], int lane) {
+  const bool h = lane & 16, g = lane & 8;
+  const FT y0 = __shfl_xor_sync(0xffffffffu, h ? s[0] : s[2], 16);
+  const FT y1 = __shfl_xor_sync(0xffffffffu, h ? s[1] : s[3], 16);
+  const FT t0 = (h ? s[2] : s[0]) + y0;  // column 2h
+  const FT t1 = (h ? s[3] : s[1]) + y1;  // column 2h + 1
+  const FT y = __shfl_xor_sync(0xffffffffu, g ? t0 : t1, 8);
+  FT u = (g ? t1 : t0) + y;  // column 2h + g
+  u += __shfl_xor_sync(0xffffffffu, u, 4);
+  u += __shfl_xor_sync(0xffffffffu, u, 2);
+  u += __shfl_xor_sync(0xffffffffu, u, 1);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) s[c] = __shfl_sync(0xffffffffu, u, (c >> 1) * 16 + (c & 1) * 8);
+}
+
 // QR of columns [0, k) over rows [0, rend), applied to columns < cend.
 // One reflector per step; column c is owned by warp c % NW, and the owner of
 // column j+1 generates reflector j+1 right after applying H_j to it
@@ -308,10 +328,8 @@ __device__ __forceinline__ void qr_stage(FT* M, int ld, int rend, int k, int cen
         }
         FT cj[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          s[u] = warp_sum(s[u]);
-          cj[u] = cc[u][j];
-        }
+        for (int u = 0; u < 4; ++u) cj[u] = cc[u][j];
+        warp_sum4(s, lane);
         __syncwarp();  // every lane has read cc[u][j] before lane 0 rewrites it
         FT su[4];
         bool live[4];

@@ -94,10 +94,48 @@ enum Slot {
 // ====================== reflector-factor vector applies =====================
 // QR-type factor Q = H_0 ... H_{k-1}; H_j = I - tau_j v v^T, v = [1; M[j+1:rend, j]]
 // (householder.hpp:114-129).  One warp; x in shared memory.
+//
+// Reflectors go two at a time: one pass over the rows accumulates v1.x, v2.x
+// and v1.v2, then x -= b1 v1 + b2 v2 with b1 = t1 (v1.x), b2 = t2 (v2.x -
+// b1 v1.v2) -- the same product H2 H1 x with one warp reduction and one
+// update sweep per pair instead of per reflector.
 template <class FT, class CT>
 __device__ void qrf_apply(const FT* M, int ld, const FT* tau, int k, int rend, CT* x, bool herm,
                           int lane) {
-  for (int s = 0; s < k; ++s) {
+  int s0 = 0;
+  for (; s0 + 1 < k; s0 += 2) {
+    const int j1 = herm ? s0 : (k - 1 - s0), j2 = herm ? s0 + 1 : (k - 2 - s0);
+    const CT t1 = CT(tau[j1]), t2 = CT(tau[j2]);
+    const int lo = j1 < j2 ? j1 : j2, hi = lo + 1;
+    const FT* v1 = M + size_t(j1) * ld;
+    const FT* v2 = M + size_t(j2) * ld;
+    CT a1 = CT(0), a2 = CT(0), gg = CT(0);
+    for (int i = hi + 1 + lane; i < rend; i += 32) {
+      const CT xi = x[i], e1 = CT(v1[i]), e2 = CT(v2[i]);
+      a1 += e1 * xi;
+      a2 += e2 * xi;
+      gg += e1 * e2;
+    }
+    const CT xlo = x[lo], xhi = hi < rend ? x[hi] : CT(0);
+    const CT mh = hi < rend ? CT(M[hi + size_t(lo) * ld]) : CT(0);  // v_lo at row hi
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    gg = warp_sum(gg);
+    // full dots: v_lo = [1 at lo, mh at hi, ...], v_hi = [0 at lo, 1 at hi, ...]
+    const bool f_lo = j1 == lo;
+    const CT dlo = (f_lo ? a1 : a2) + xlo + mh * xhi, dhi = (f_lo ? a2 : a1) + xhi;
+    const CT d1 = f_lo ? dlo : dhi, d2 = f_lo ? dhi : dlo;
+    const CT b1 = t1 * d1, b2 = t2 * (d2 - b1 * (gg + mh));
+    const CT blo = f_lo ? b1 : b2, bhi = f_lo ? b2 : b1;
+    __syncwarp();
+    if (lane == 0) {
+      x[lo] = xlo - blo;
+      if (hi < rend) x[hi] = xhi - (blo * mh + bhi);
+    }
+    for (int i = hi + 1 + lane; i < rend; i += 32) x[i] -= b1 * CT(v1[i]) + b2 * CT(v2[i]);
+    __syncwarp();
+  }
+  for (int s = s0; s < k; ++s) {
     const int j = herm ? s : (k - 1 - s);
     const CT t = CT(tau[j]);
     if (t == CT(0)) continue;
@@ -115,10 +153,46 @@ __device__ void qrf_apply(const FT* M, int ld, const FT* tau, int k, int rend, C
 
 // RQ-type factor Z = H_0 ... H_{kk-1}; reflector j lives in row rtop+j, entries
 // at columns c0+t for t < ptop+j, unit at t = ptop+j (householder.hpp:202-222).
+// Two reflectors per step as in qrf_apply (columns reversed: v_lo has its
+// unit at pc_lo, v_hi its unit at pc_lo + 1 and a stored entry at pc_lo).
 template <class FT, class CT>
 __device__ void rqf_apply(const FT* M, int ld, const FT* tau, int kk, int rtop, int c0, int ptop,
                           CT* x, bool herm, int lane) {
-  for (int s = 0; s < kk; ++s) {
+  int s0 = 0;
+  for (; s0 + 1 < kk; s0 += 2) {
+    const int j1 = herm ? s0 : (kk - 1 - s0), j2 = herm ? s0 + 1 : (kk - 2 - s0);
+    const CT t1 = CT(tau[j1]), t2 = CT(tau[j2]);
+    const int jl = j1 < j2 ? j1 : j2;
+    const int pl = ptop + jl, ph = pl + 1;
+    const FT* v1 = M + (rtop + j1) + size_t(c0) * ld;
+    const FT* v2 = M + (rtop + j2) + size_t(c0) * ld;
+    CT a1 = CT(0), a2 = CT(0), gg = CT(0);
+    for (int q = lane; q < pl; q += 32) {
+      const CT xq = x[q], e1 = CT(v1[size_t(q) * ld]), e2 = CT(v2[size_t(q) * ld]);
+      a1 += e1 * xq;
+      a2 += e2 * xq;
+      gg += e1 * e2;
+    }
+    const bool f_lo = j1 == jl;
+    const CT xl = x[pl], xh = x[ph];
+    const CT mh = CT((f_lo ? v2 : v1)[size_t(pl) * ld]);  // v_hi at column pl
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    gg = warp_sum(gg);
+    const CT dlo = (f_lo ? a1 : a2) + xl, dhi = (f_lo ? a2 : a1) + mh * xl + xh;
+    const CT d1 = f_lo ? dlo : dhi, d2 = f_lo ? dhi : dlo;
+    const CT b1 = t1 * d1, b2 = t2 * (d2 - b1 * (gg + mh));
+    const CT blo = f_lo ? b1 : b2, bhi = f_lo ? b2 : b1;
+    __syncwarp();
+    if (lane == 0) {
+      x[pl] = xl - (blo + bhi * mh);
+      x[ph] = xh - bhi;
+    }
+    for (int q = lane; q < pl; q += 32)
+      x[q] -= b1 * CT(v1[size_t(q) * ld]) + b2 * CT(v2[size_t(q) * ld]);
+    __syncwarp();
+  }
+  for (int s = s0; s < kk; ++s) {
     const int j = herm ? s : (kk - 1 - s);
     const CT t = CT(tau[j]);
     if (t == CT(0)) continue;

@@ -213,9 +213,27 @@ __device__ void rqf_apply(const FT* M, int ld, const FT* tau, int kk, int rtop, 
 // U = M[r0:r0+k, c0:c0+k] upper triangular; x overwritten.  Returns false and
 // sets *bad to the block-relative pivot index on an exact zero pivot, in the
 // same sweep order as trsv_sub (matrix.hpp:242-267).
+// Columns go two at a time (same operations in the same order as one at a
+// time, so bitwise equal): one update sweep and two warp syncs per pair.
 template <class FT, class CT>
 __device__ bool trsv_n(const FT* M, int ld, int r0, int c0, int k, CT* x, int lane, int* bad) {
-  for (int jj = k - 1; jj >= 0; --jj) {
+  int jj = k - 1;
+  for (; jj >= 1; jj -= 2) {
+    const FT* col = M + size_t(c0 + jj) * ld + r0;
+    const FT* cl1 = col - ld;
+    const CT piv = CT(col[jj]), piv1 = CT(cl1[jj - 1]);
+    if (piv == CT(0) || piv1 == CT(0)) break;  // the single-column loop reports it
+    const CT xj = x[jj] / piv;
+    const CT xj1 = (x[jj - 1] - xj * CT(col[jj - 1])) / piv1;
+    __syncwarp();
+    if (lane == 0) {
+      x[jj] = xj;
+      x[jj - 1] = xj1;
+    }
+    for (int i = lane; i < jj - 1; i += 32) x[i] = (x[i] - xj * CT(col[i])) - xj1 * CT(cl1[i]);
+    __syncwarp();
+  }
+  for (; jj >= 0; --jj) {
     const FT* col = M + size_t(c0 + jj) * ld + r0;
     const CT piv = CT(col[jj]);
     if (piv == CT(0)) {
@@ -234,7 +252,24 @@ __device__ bool trsv_n(const FT* M, int ld, int r0, int c0, int k, CT* x, int la
 // U^T x = b as a forward column sweep over the rows of U
 template <class FT, class CT>
 __device__ bool trsv_t(const FT* M, int ld, int r0, int c0, int k, CT* x, int lane, int* bad) {
-  for (int j = 0; j < k; ++j) {
+  int j = 0;
+  for (; j + 1 < k; j += 2) {
+    const FT* row = M + (r0 + j) + size_t(c0) * ld;
+    const FT* rw1 = row + 1;
+    const CT piv = CT(row[size_t(j) * ld]), piv1 = CT(rw1[size_t(j + 1) * ld]);
+    if (piv == CT(0) || piv1 == CT(0)) break;  // the single-row loop reports it
+    const CT xj = x[j] / piv;
+    const CT xj1 = (x[j + 1] - CT(row[size_t(j + 1) * ld]) * xj) / piv1;
+    __syncwarp();
+    if (lane == 0) {
+      x[j] = xj;
+      x[j + 1] = xj1;
+    }
+    for (int i = j + 2 + lane; i < k; i += 32)
+      x[i] = (x[i] - CT(row[size_t(i) * ld]) * xj) - CT(rw1[size_t(i) * ld]) * xj1;
+    __syncwarp();
+  }
+  for (; j < k; ++j) {
     const FT* row = M + (r0 + j) + size_t(c0) * ld;
     const CT piv = CT(row[size_t(j) * ld]);
     if (piv == CT(0)) {

@@ -343,7 +343,9 @@ __device__ void gen_col_reflector(FT* col, int j, int rend, FT* tau_j, int lane)
     return;
   }
   const double a = double(alpha);
-  const double beta = -copysign(hypot(a, xn), a);
+  // binary32 data cannot overflow a binary64 a^2 + ss: one sqrt instead of
+  // sqrt + hypot on the reflector chain
+  const double beta = -copysign(sizeof(FT) == 4 ? sqrt(fma(a, a, ss)) : hypot(a, xn), a);
   const FT tj = FT((beta - a) / beta);
   const FT inv = FT(1.0 / (a - beta));
   for (int i = j + 1 + lane; i < rend; i += 32) col[i] = col[i] * inv;
@@ -485,7 +487,7 @@ __device__ __forceinline__ void rq_stage(FT* M, int ld, int rb, int rr, int c0, 
       FT tj = FT(0), beta = alpha;
       if (xn != 0.0) {
         const double a = double(alpha);
-        const double bt = -copysign(hypot(a, xn), a);
+        const double bt = -copysign(sizeof(FT) == 4 ? sqrt(fma(a, a, ss)) : hypot(a, xn), a);
         tj = FT((bt - a) / bt);
         const FT inv = FT(1.0 / (a - bt));
         for (int q = lane; q < pc; q += 32) vrow[size_t(q) * ld] = vrow[size_t(q) * ld] * inv;

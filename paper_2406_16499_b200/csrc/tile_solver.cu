@@ -377,6 +377,49 @@ __device__ __forceinline__ void warp_sum4(FT s[4], int lane) {
   for (int c = 0; c < 4; ++c) s[c] = __shfl_sync(0xffffffffu, u, (c >> 1) * 16 + (c & 1) * 8);
 }
 
+// H_j applied to a group of CG columns c, c+NW, ... of one warp (columns past
+// cend are clamped and not written): one pass for the CG dots, one
+// transposed reduction per four columns, one update pass.
+template <class FT, int CG>
+__device__ __forceinline__ void qr_cols(FT* M, int ld, const FT* v, int c, int cend, int j,
+                                        int rend, FT tj, int lane) {
+  FT s[CG];
+  FT* cc[CG];
+#pragma unroll
+  for (int u = 0; u < CG; ++u) {
+    s[u] = FT(0);
+    cc[u] = M + size_t(min(c + u * NW, cend - 1)) * ld;
+  }
+#pragma unroll 4
+  for (int i = j + 1 + lane; i < rend; i += 32) {
+    const FT vi = v[i];
+#pragma unroll
+    for (int u = 0; u < CG; ++u) s[u] += vi * cc[u][i];
+  }
+  FT cj[CG];
+#pragma unroll
+  for (int u = 0; u < CG; ++u) cj[u] = cc[u][j];
+#pragma unroll
+  for (int g = 0; g < CG; g += 4) warp_sum4(s + g, lane);
+  __syncwarp();  // every lane has read cc[u][j] before lane 0 rewrites it
+  bool live[CG];
+#pragma unroll
+  for (int u = 0; u < CG; ++u) {
+    live[u] = c + u * NW < cend;
+    s[u] = (s[u] + cj[u]) * tj;
+    if (lane == 0 && live[u]) cc[u][j] = cj[u] - s[u];
+  }
+  // one pass over the rows for all columns: v[i] read once, the column loads
+  // independent of each other (no per-column latency chain)
+#pragma unroll 4
+  for (int i = j + 1 + lane; i < rend; i += 32) {
+    const FT vi = v[i];
+#pragma unroll
+    for (int u = 0; u < CG; ++u)
+      if (live[u]) cc[u][i] -= s[u] * vi;
+  }
+}
+
 // QR of columns [0, k) over rows [0, rend), applied to columns < cend.
 // One reflector per step; column c is owned by warp c % NW, and the owner of
 // column j+1 generates reflector j+1 right after applying H_j to it
@@ -388,7 +431,7 @@ __device__ __forceinline__ void warp_sum4(FT s[4], int lane) {
 // j+1 never waits for the slowest warp's bulk updates.  Every warp owns a
 // column every NW steps, so no warp lags more than NW steps: a ring of 2 NW
 // barriers cannot wrap onto a pending phase.
-template <class FT>
+template <class FT, bool WIDE = false>
 __device__ __forceinline__ void qr_stage(FT* M, int ld, int rend, int k, int cend, FT* tau, int warp, int lane) {
   if (k <= 0) return;
   constexpr int NQB = 2 * NW;
@@ -426,40 +469,11 @@ __device__ __forceinline__ void qr_stage(FT* M, int ld, int rend, int k, int cen
       c += NW;
     }
     if (tj != FT(0)) {
-      for (; c < cend; c += 4 * NW) {
-        FT s[4] = {FT(0), FT(0), FT(0), FT(0)};
-        FT* cc[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) cc[u] = M + size_t(min(c + u * NW, cend - 1)) * ld;
-#pragma unroll 4
-        for (int i = j + 1 + lane; i < rend; i += 32) {
-          const FT vi = v[i];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) s[u] += vi * cc[u][i];
-        }
-        FT cj[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) cj[u] = cc[u][j];
-        warp_sum4(s, lane);
-        __syncwarp();  // every lane has read cc[u][j] before lane 0 rewrites it
-        FT su[4];
-        bool live[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          live[u] = c + u * NW < cend;
-          su[u] = (s[u] + cj[u]) * tj;
-          if (lane == 0 && live[u]) cc[u][j] = cj[u] - su[u];
-        }
-        // one pass over the rows for the four columns: v[i] read once, the
-        // column loads independent of each other (no per-column latency chain)
-#pragma unroll 4
-        for (int i = j + 1 + lane; i < rend; i += 32) {
-          const FT vi = v[i];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (live[u]) cc[u][i] -= su[u] * vi;
-        }
-      }
+      // eight binary32 columns fit the register budget with shared-memory
+      // (32-bit) addressing; 64-bit global pointers would spill
+      if constexpr (WIDE && sizeof(FT) == 4)
+        for (; c + 7 * NW < cend; c += 8 * NW) qr_cols<FT, 8>(M, ld, v, c, cend, j, rend, tj, lane);
+      for (; c < cend; c += 4 * NW) qr_cols<FT, 4>(M, ld, v, c, cend, j, rend, tj, lane);
     }
   }
   __syncthreads();
@@ -750,9 +764,9 @@ __global__ void __launch_bounds__(NT, 1) tile_solve_kernel(TileArgs a) {
   // ---------------- GRQ / GQR at u_f ------------------------------------------
   if (KIND == KIND_LSE) {
     rq_stage<FT>(M, ld, m, p, 0, n, tau2, scal, tid, warp, lane);
-    qr_stage<FT>(M, ld, m, m < n ? m : n, n, tau1, warp, lane);
+    qr_stage<FT, !MG>(M, ld, m, m < n ? m : n, n, tau1, warp, lane);
   } else {
-    qr_stage<FT>(M, ld, n, m, m + p, tau1, warp, lane);
+    qr_stage<FT, !MG>(M, ld, n, m, m + p, tau1, warp, lane);
     if (a.stamps && pid == 0 && tid == 0) a.stamps[30] = globaltimer_ns();  // debug: QR stage done
     rq_stage<FT>(M, ld, 0, n, m, p, tau2, scal, tid, warp, lane);
     if (a.stamps && pid == 0 && tid == 0) a.stamps[31] = globaltimer_ns();  // debug: RQ stage done

@@ -142,6 +142,52 @@ def _matrix_ld(M):
     return rows, cols, max(rows, 1)
 
 
+def _dev_inputs(mats, vecs, shapes, what):
+    """Validate the CUDA-tensor inputs of a single solve before they reach the C
+    ABI: binary64, one device, 2-D column-major matrices, vectors of the right
+    length with unit stride (made contiguous).  Wrong input here would be read
+    out of bounds on the device.  Returns the (possibly contiguous) vectors."""
+    import torch
+
+    dev = mats[0].device
+    for t in list(mats) + list(vecs):
+        if not _is_cuda(t):
+            raise _capi.InvalidInput(f"{what}: mixing CUDA tensors and host arrays")
+        if t.device != dev:
+            raise _capi.InvalidInput(f"{what}: inputs on different devices")
+        if t.dtype != torch.float64:
+            raise _capi.InvalidInput(f"{what}: CUDA inputs must be torch.float64 (got {t.dtype})")
+    for M in mats:
+        if M.dim() != 2:
+            raise _capi.DimensionError(f"{what}: matrices must be 2-D")
+    out = []
+    for v, n in zip(vecs, shapes):
+        if v.dim() != 1 or v.shape[0] != n:
+            raise _capi.DimensionError(f"{what}: rhs length mismatch")
+        out.append(v if v.stride(0) == 1 else v.contiguous())
+    return out
+
+
+def _dev_lse(pb, what="lse_problem"):
+    A, B = pb.A, pb.B
+    if A.dim() != 2 or B.dim() != 2 or A.shape[1] != B.shape[1]:
+        raise _capi.DimensionError(f"{what}: A and B column counts differ")
+    b, d = _dev_inputs((A, B), (pb.b, pb.d), (A.shape[0], B.shape[0]), what)
+    m, n, lda = _matrix_ld(A)
+    p, _, ldb = _matrix_ld(B)
+    return A, B, b, d, m, n, p, lda, ldb
+
+
+def _dev_gls(pb, what="gls_problem"):
+    W, V = pb.W, pb.V
+    if W.dim() != 2 or V.dim() != 2 or W.shape[0] != V.shape[0]:
+        raise _capi.DimensionError(f"{what}: W and V row counts differ")
+    (d,) = _dev_inputs((W, V), (pb.d,), (W.shape[0],), what)
+    n, m, ldw = _matrix_ld(W)
+    _, p, ldv = _matrix_ld(V)
+    return W, V, d, n, m, p, ldw, ldv
+
+
 def _trace_from(tr: Trace, hist: np.ndarray) -> RefinementTrace:
     it = int(tr.iterations)
     return RefinementTrace(_STATUS.get(tr.status, str(tr.status)), it,
@@ -158,9 +204,7 @@ def mplse(pb: LseProblem, cfg: RefinementConfig | None = None, stream=None) -> M
     if dev:
         import torch
 
-        A, B, b, d = pb.A, pb.B, pb.b, pb.d
-        m, n, lda = _matrix_ld(A)
-        p, _, ldb = _matrix_ld(B)
+        A, B, b, d, m, n, p, lda, ldb = _dev_lse(pb)
         x = torch.empty(n, dtype=torch.float64, device=A.device)
         r = torch.empty(m, dtype=torch.float64, device=A.device)
         v = torch.empty(p, dtype=torch.float64, device=A.device)
@@ -199,9 +243,7 @@ def mpgls(pb: GlsProblem, cfg: RefinementConfig | None = None, stream=None) -> M
     if dev:
         import torch
 
-        W, V, d = pb.W, pb.V, pb.d
-        n, m, ldw = _matrix_ld(W)
-        _, p, ldv = _matrix_ld(V)
+        W, V, d, n, m, p, ldw, ldv = _dev_gls(pb)
         x = torch.empty(m, dtype=torch.float64, device=W.device)
         y = torch.empty(p, dtype=torch.float64, device=W.device)
         z = torch.empty(n, dtype=torch.float64, device=W.device)
@@ -244,9 +286,7 @@ def gmres_refine_lse(pb: LseProblem, cfg: RefinementConfig | None = None,
     if dev:
         import torch
 
-        A, B, b, d = pb.A, pb.B, pb.b, pb.d
-        m, n, lda = _matrix_ld(A)
-        p, _, ldb = _matrix_ld(B)
+        A, B, b, d, m, n, p, lda, ldb = _dev_lse(pb)
         x = torch.empty(n, dtype=torch.float64, device=A.device)
         r = torch.empty(m, dtype=torch.float64, device=A.device)
         v = torch.empty(p, dtype=torch.float64, device=A.device)
@@ -288,9 +328,7 @@ def gmres_refine_gls(pb: GlsProblem, cfg: RefinementConfig | None = None,
     if dev:
         import torch
 
-        W, V, d = pb.W, pb.V, pb.d
-        n, m, ldw = _matrix_ld(W)
-        _, p, ldv = _matrix_ld(V)
+        W, V, d, n, m, p, ldw, ldv = _dev_gls(pb)
         x = torch.empty(m, dtype=torch.float64, device=W.device)
         y = torch.empty(p, dtype=torch.float64, device=W.device)
         z = torch.empty(n, dtype=torch.float64, device=W.device)
@@ -325,9 +363,7 @@ def lse_direct(pb: LseProblem, stream=None) -> LseState:
     if dev:
         import torch
 
-        A, B, b, d = pb.A, pb.B, pb.b, pb.d
-        m, n, lda = _matrix_ld(A)
-        p, _, ldb = _matrix_ld(B)
+        A, B, b, d, m, n, p, lda, ldb = _dev_lse(pb)
         x = torch.empty(n, dtype=torch.float64, device=A.device)
         r = torch.empty(m, dtype=torch.float64, device=A.device)
         v = torch.empty(p, dtype=torch.float64, device=A.device)
@@ -359,9 +395,7 @@ def gls_direct(pb: GlsProblem, stream=None) -> GlsState:
     if dev:
         import torch
 
-        W, V, d = pb.W, pb.V, pb.d
-        n, m, ldw = _matrix_ld(W)
-        _, p, ldv = _matrix_ld(V)
+        W, V, d, n, m, p, ldw, ldv = _dev_gls(pb)
         x = torch.empty(m, dtype=torch.float64, device=W.device)
         y = torch.empty(p, dtype=torch.float64, device=W.device)
         z = torch.empty(n, dtype=torch.float64, device=W.device)
@@ -423,6 +457,18 @@ def _batch_common(kind, A, B, rhs1, rhs2, cfg, stream, history):
         rhs2 = np.ascontiguousarray(rhs2, dtype=np.float64)
         if rhs1 is not None:
             rhs1 = np.ascontiguousarray(rhs1, dtype=np.float64)
+    if dev:
+        import torch
+
+        for t in (A, B, rhs1, rhs2):
+            if t is None:
+                continue
+            if not _is_cuda(t) or t.device != A.device:
+                raise _capi.InvalidInput("batched: all inputs must be CUDA tensors on one device")
+            if t.dtype != torch.float64:
+                raise _capi.InvalidInput(f"batched: CUDA inputs must be torch.float64 (got {t.dtype})")
+        if A.dim() != 3 or B.dim() != 3:
+            raise _capi.DimensionError("batched: matrices must be (batch, rows, cols)")
     bt, ra, ca, lda, sA = _batched_layout(A)
     bt2, rb, cb, ldb, sB = _batched_layout(B)
     if bt2 != bt:
@@ -430,9 +476,22 @@ def _batch_common(kind, A, B, rhs1, rhs2, cfg, stream, history):
     if kind == "lse":
         m, n, p = ra, ca, rb
         nx, nr, nv = n, m, p
+        if cb != n:
+            raise _capi.DimensionError("lse_problem: A and B column counts differ")
     else:
         n, m, p = ra, ca, cb
         nx, nr, nv = m, p, n
+        if rb != n:
+            raise _capi.DimensionError("gls_problem: W and V row counts differ")
+    want = ((rhs1, m), (rhs2, p)) if kind == "lse" else ((rhs2, n),)
+    for t, ln in want:
+        if tuple(t.shape) != (bt, ln):
+            raise _capi.DimensionError("batched: rhs shape mismatch")
+    if dev:
+        if rhs1 is not None and rhs1.stride(1) != 1:
+            rhs1 = rhs1.contiguous()
+        if rhs2.stride(1) != 1:
+            rhs2 = rhs2.contiguous()
 
     def vstride(t):
         if t is None:

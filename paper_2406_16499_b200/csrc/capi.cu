@@ -493,6 +493,14 @@ int run(const Shape& s, int64_t batch, const double* A, int64_t lda, int64_t sA,
     if ((e = bgws.alloc(per * size_t(batch), st))) return cuda_fail(e, "cudaMallocAsync(workspace)");
     a.gws = bgws.p;
   }
+  // defined outputs for every problem: history rows past a problem's pass count
+  // read 0, and a problem the kernel rejects (errcode != 0) reports 0 passes
+  // and status -1 instead of stale memory
+  if (a.hist && (e = cudaMemsetAsync(a.hist, 0, sizeof(double) * batch * cfg->maxit * 3, st)))
+    return cuda_fail(e, "cudaMemsetAsync(history)");
+  if ((a.iters && (e = cudaMemsetAsync(a.iters, 0, sizeof(int64_t) * batch, st))) ||
+      (a.status && (e = cudaMemsetAsync(a.status, 0xff, sizeof(int32_t) * batch, st))))
+    return cuda_fail(e, "cudaMemsetAsync(status)");
   if ((e = use_reg ? mlsb::launch_lse_reg(a, st) : mlsb::launch_tile_solver(a, st)))
     return cuda_fail(e, "tile solver launch");
 

@@ -1529,8 +1529,25 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
     cudaEventRecord(e2, st);
     pev.emplace_back(name, e2);
   };
+  // per-pass phase events: [pass start, correction start, correction end]
+  // -> trace.timing.residual (residual + stop test) and .correction | .gmres
+  // (refine.hpp:45-52; lse.hpp:387, :416)
+  std::vector<cudaEvent_t> pph;
+  auto pmark = [&]() {
+    cudaEvent_t e3;
+    cudaEventCreate(&e3);
+    cudaEventRecord(e3, st);
+    pph.push_back(e3);
+  };
+  struct PphGuard {
+    std::vector<cudaEvent_t>& v;
+    ~PphGuard() {
+      for (auto x : v) cudaEventDestroy(x);
+    }
+  } pph_guard{pph};
   for (pass = 1; pass <= P.maxit; ++pass) {
     mark("start");
+    pmark();
     // row initialisers and weights of this pass
     if (lse) {
       k_sub<WT><<<nblk(m), KT, 0, st>>>(rinit, sw, m, rrow);                  // b - r
@@ -1632,6 +1649,7 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       break;
     }
 
+    pmark();  // correction (or GMRES) starts
     if constexpr (kGm) {
       if (P.gmres) {
         int64_t its = 0;
@@ -1645,6 +1663,7 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
                                             flags + 3, &its, st);
         if (rc) return rc;
         out->inner += its;
+        pmark();
         continue;
       }
     }
@@ -1735,6 +1754,7 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       k_promote_add<WT, CT><<<nblk(n), KT, 0, st>>>(sw, n, u, sb, true, flags + 3);  // dz = -Q h
     }
     if ((e = cudaGetLastError())) return MLSB_ERR_CUDA;
+    pmark();
     mark("update");
     if (loop_prof && pass == 1) {
       cudaStreamSynchronize(st);
@@ -1774,9 +1794,29 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   out->phases[5] = (ms[0] + ms[4]) * 1e-3;  // other
   out->phases[0] = ms[1] * 1e-3;            // factorization
   out->phases[1] = ms[2] * 1e-3;            // init
-  out->phases[P.gmres ? 4 : 2] = ms[3] * 1e-3;  // the refinement loop (residual + correction | gmres)
-  out->phases[3] = 0.0;
-  out->phases[4] = 0.0;
+  // the loop split per pass: [start, corr) = residual + stop test, [corr, end)
+  // = correction (classical) or GMRES; a pass that stopped has no correction
+  double res_ms = 0.0, cor_ms = 0.0;
+  for (size_t i = 0; i < pph.size(); i += 3) {
+    float a = 0.f, b2 = 0.f;
+    const bool has_corr = i + 2 < pph.size() || (i + 2 == pph.size() - 0 && false);
+    if (i + 1 < pph.size()) {
+      cudaEventElapsedTime(&a, pph[i], pph[i + 1]);
+      if (i + 2 < pph.size()) cudaEventElapsedTime(&b2, pph[i + 1], pph[i + 2]);
+    } else {  // final pass: residual + stop test up to the loop's end event
+      cudaEventElapsedTime(&a, pph[i], ev[4]);
+    }
+    (void)has_corr;
+    res_ms += a;
+    cor_ms += b2;
+  }
+  // whatever of the loop interval the per-pass events do not cover (host-side
+  // gaps between passes are on the device timeline too) goes to "residual"
+  const double rest = ms[3] - res_ms - cor_ms;
+  if (rest > 0.0) res_ms += rest;
+  out->phases[2] = res_ms * 1e-3;                  // residual (+ stop test)
+  out->phases[3] = P.gmres ? 0.0 : cor_ms * 1e-3;  // correction
+  out->phases[4] = P.gmres ? cor_ms * 1e-3 : 0.0;  // gmres
   for (auto& x : ev) cudaEventDestroy(x);
   out->status = status;
   out->iters = pass;

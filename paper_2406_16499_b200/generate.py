@@ -13,7 +13,8 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["haar", "svd_matrix", "lse_problem", "gls_problem", "lse_batch_torch", "CONFIGS"]
+__all__ = ["haar", "svd_matrix", "lse_problem", "gls_problem", "lse_batch_torch", "lse_batch_numpy",
+           "block_seed", "GEN_BLOCK", "CONFIGS"]
 
 
 def haar(rng: np.random.Generator, rows: int, cols: int, cplx: bool = False) -> np.ndarray:
@@ -65,23 +66,42 @@ def gls_problem(n, m, p, kappa_A, kappa_B, seed, cplx=False):
     return W, V, _rhs(rng, n, cplx)
 
 
+GEN_BLOCK = 1024  # problems per generator block (lse_batch_torch)
+
+
+def block_seed(seed: int, block: int) -> int:
+    """Seed of generator block `block` (problems block*GEN_BLOCK ...) of a batch
+    with base seed `seed`: any slice of the batch can be regenerated on its own."""
+    return seed * 1_000_003 + block
+
+
 def lse_batch_torch(batch, m, n, p, log10_kappa_range=(1.0, 5.0), kappa_B=10.0, seed=1000,
-                    device="cuda", chunk=4096):
-    """Batched BASELINE config 4 on the device: per problem kappa(A) = 10^U(1,5),
-    kappa(B) = 10.  Returns A (batch, m, n), B (batch, p, n) column-major per
-    problem, b (batch, m), d (batch, p), kappa_A (batch,)."""
+                    device="cuda", start=0):
+    """Batched BASELINE config 4: per problem kappa(A) = 10^U(1,5), kappa(B) = 10.
+    Returns problems [start, start + batch) of the batch with base seed `seed`:
+    A (batch, m, n), B (batch, p, n) column-major per problem, b (batch, m),
+    d (batch, p), kappa_A (batch,).
+
+    The batch is cut into fixed blocks of GEN_BLOCK problems; block j draws
+    everything from its own generator (block_seed(seed, j)) with the same call
+    shapes whatever the slice, so a slice is bitwise the same problems as in
+    the whole batch on the same device type.  That is what lets a rank of the
+    sharded bench generate only its shard, and the reference arm regenerate
+    the GPU arm's first problems (SURVEY.md §8(e) seed rule, per block rather
+    than per problem)."""
     import torch
 
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
     f64 = torch.float64
     A = torch.empty((batch, n, m), dtype=f64, device=device).transpose(1, 2)
     B = torch.empty((batch, n, p), dtype=f64, device=device).transpose(1, 2)
+    b = torch.empty((batch, m), dtype=f64, device=device)
+    d = torch.empty((batch, p), dtype=f64, device=device)
+    kA = torch.empty(batch, dtype=f64, device=device)
     lo, hi = log10_kappa_range
-    kA = 10.0 ** (lo + (hi - lo) * torch.rand(batch, generator=g, device=device, dtype=f64))
+    nb = GEN_BLOCK
 
-    def haar_t(bs, rows, cols):
-        G = torch.randn((bs, rows, cols), generator=g, device=device, dtype=f64)
+    def haar_t(g, rows, cols):
+        G = torch.randn((nb, rows, cols), generator=g, device=device, dtype=f64)
         Q, R = torch.linalg.qr(G)
         s = torch.sign(torch.diagonal(R, dim1=-2, dim2=-1))
         s[s == 0] = 1
@@ -93,18 +113,28 @@ def lse_batch_torch(batch, m, n, p, log10_kappa_range=(1.0, 5.0), kappa_B=10.0, 
         t = torch.arange(k, dtype=f64, device=device) / (k - 1)
         return kap[:, None] ** (-t[None, :])
 
-    for s0 in range(0, batch, chunk):
-        s1 = min(batch, s0 + chunk)
-        bs = s1 - s0
+    for blk in range(start // nb, (start + batch + nb - 1) // nb):
+        g = torch.Generator(device=device)
+        g.manual_seed(block_seed(seed, blk))
+        ka_blk = 10.0 ** (lo + (hi - lo) * torch.rand(nb, generator=g, device=device, dtype=f64))
         ka = min(m, n)
-        UA, VA = haar_t(bs, m, ka), haar_t(bs, n, ka)
-        A[s0:s1] = (UA * sig(ka, kA[s0:s1])[:, None, :]) @ VA.transpose(1, 2)
+        UA, VA = haar_t(g, m, ka), haar_t(g, n, ka)
+        A_blk = (UA * sig(ka, ka_blk)[:, None, :]) @ VA.transpose(1, 2)
         kb = min(p, n)
-        UB, VB = haar_t(bs, p, kb), haar_t(bs, n, kb)
-        kBv = torch.full((bs,), float(kappa_B), dtype=f64, device=device)
-        B[s0:s1] = (UB * sig(kb, kBv)[:, None, :]) @ VB.transpose(1, 2)
-    b = torch.randn((batch, m), generator=g, device=device, dtype=f64)
-    d = torch.randn((batch, p), generator=g, device=device, dtype=f64)
+        UB, VB = haar_t(g, p, kb), haar_t(g, n, kb)
+        kBv = torch.full((nb,), float(kappa_B), dtype=f64, device=device)
+        B_blk = (UB * sig(kb, kBv)[:, None, :]) @ VB.transpose(1, 2)
+        b_blk = torch.randn((nb, m), generator=g, device=device, dtype=f64)
+        d_blk = torch.randn((nb, p), generator=g, device=device, dtype=f64)
+        g0 = blk * nb                       # global index of the block's first problem
+        s0, s1 = max(start, g0), min(start + batch, g0 + nb)
+        o, i = s0 - start, s0 - g0          # output / in-block offsets
+        c = s1 - s0
+        A[o:o + c] = A_blk[i:i + c]
+        B[o:o + c] = B_blk[i:i + c]
+        b[o:o + c] = b_blk[i:i + c]
+        d[o:o + c] = d_blk[i:i + c]
+        kA[o:o + c] = ka_blk[i:i + c]
     return A, B, b, d, kA
 
 

@@ -13,8 +13,7 @@ host side, around the GPU solvers.
 
 Methods: ``"direct"``, ``"ir"`` (classical IR, mplse / mpgls) and, for LSE,
 ``"gmres-left"`` / ``"gmres-bd"`` (GMRES-IR, gmres_refine_lse / gmres_refine_gls,
-inc/krylov.hpp:545-689).  GMRES-IR for GLS is not built on the GPU yet: it
-reports status ``"unsupported"``.
+inc/krylov.hpp:545-784), for LSE and GLS.
 """
 from __future__ import annotations
 

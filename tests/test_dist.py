@@ -70,3 +70,43 @@ def test_two_rank_gloo_shard_solve_gather(tmp_path, port):
     assert np.array_equal(x, np.concatenate(xs))
     A, B, b, d, _ = G.lse_batch_numpy(total, 12, 6, 2, seed=1000)
     assert np.array_equal(x, port.mplse_batch(A, B, b, d)[0])
+
+
+def _gpu_worker(rank, world, port, total, out_dir):
+    """One rank of the sharded batch on the GPU: generate only the shard (per-block
+    seeds), solve it through mplse_batched, gather to rank 0 (gloo over host
+    copies: both ranks share the one GPU of the test box, and neither waits on
+    the other's kernels)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2406_16499_b200 as P
+        from paper_2406_16499_b200 import generate as G
+
+        torch.cuda.set_device(0)
+        sh = shard_plan(total, world, rank)
+        A, B, b, d, _ = G.lse_batch_torch(sh.count, 256, 128, 32, seed=1000, device="cuda", start=sh.start)
+        out = P.mplse_batched(A, B, b, d)
+        torch.cuda.synchronize()
+        counts = [shard_plan(total, world, r).count for r in range(world)]
+        full = gather_rows_to_rank0(out.x.cpu(), counts)
+        its = gather_rows_to_rank0(out.iterations.cpu(), counts)
+        if rank == 0:
+            np.save(os.path.join(out_dir, "x.npy"), full.numpy())
+            np.save(os.path.join(out_dir, "it.npy"), its.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_gpu_shards_match_single_gpu(tmp_path, gpu):
+    """the sharded batch, gathered, is bitwise the single-GPU solve."""
+    total = 3000  # shards straddle a generator block boundary (1024)
+    mp.spawn(_gpu_worker, args=(2, _free_port(), total, str(tmp_path)), nprocs=2, join=True)
+    from paper_2406_16499_b200 import generate as G
+
+    A, B, b, d, _ = G.lse_batch_torch(total, 256, 128, 32, seed=1000, device="cuda")
+    out = gpu.mplse_batched(A, B, b, d)
+    assert np.array_equal(np.load(tmp_path / "x.npy"), out.x.cpu().numpy())
+    assert np.array_equal(np.load(tmp_path / "it.npy"), out.iterations.cpu().numpy())

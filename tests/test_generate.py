@@ -46,3 +46,21 @@ def test_configs_match_baseline():
     assert (c["C3"]["m"], c["C3"]["n"], c["C3"]["p"]) == (8192, 4096, 1024)
     assert (c["C4"]["batch"], c["C4"]["m"], c["C4"]["n"], c["C4"]["p"]) == (65536, 256, 128, 32)
     assert (c["C5"]["n"], c["C5"]["m"], c["C5"]["p"]) == (4096, 2048, 3072)
+
+
+def test_batch_torch_slices_are_the_same_problems():
+    """Per-block seeds: any slice [start, start + count) of a batch regenerates
+    bitwise the same problems as the whole batch (what the sharded bench and
+    the reference arm rely on)."""
+    import torch
+
+    A, B, b, d, kA = G.lse_batch_torch(G.GEN_BLOCK + 300, 12, 6, 2, seed=11, device="cpu")
+    for start, count in ((0, 5), (G.GEN_BLOCK - 7, 20), (500, G.GEN_BLOCK - 200)):
+        A2, B2, b2, d2, k2 = G.lse_batch_torch(count, 12, 6, 2, seed=11, device="cpu", start=start)
+        sl = slice(start, start + count)
+        for full, part in ((A, A2), (B, B2), (b, b2), (d, d2), (kA, k2)):
+            assert torch.equal(full[sl], part)
+    assert A.stride() == (72, 1, 12)  # column-major per problem
+    assert np.all((kA.numpy() >= 10.0) & (kA.numpy() <= 1e5))
+    s = torch.linalg.svdvals(A[3])
+    assert float(s[0] / s[-1]) == pytest.approx(float(kA[3]), rel=1e-8)

@@ -130,6 +130,21 @@ __constant__ unsigned long long* g_probe = nullptr;
 #define PROBE1(k) do { } while (0)
 #endif
 
+// debug: per-problem dumps of intermediate state for the first DUMP_NP problems
+// (mlsb_debug_set_dump; null in production -- one predicated load per point)
+constexpr int DUMP_NP = 64, DUMP_STRIDE = 160 * 1024;  // floats per problem
+__device__ float* g_dump = nullptr;
+__device__ __forceinline__ void dump_f(int64_t pid, int off, const float* src, int n, int tid) {
+  float* d = g_dump;
+  if (d == nullptr || pid >= DUMP_NP) return;
+  for (int i = tid; i < n; i += 512) d[pid * DUMP_STRIDE + off + i] = src[i];
+}
+__device__ __forceinline__ void dump_d(int64_t pid, int off, const double* src, int n, int tid) {
+  float* d = g_dump;
+  if (d == nullptr || pid >= DUMP_NP) return;
+  for (int i = tid; i < n; i += 512) reinterpret_cast<double*>(d + pid * DUMP_STRIDE + off)[i] = src[i];
+}
+
 // ------------------------------------------- multi-warp WY block applies
 // T blocks (32 x 32, forward xLARFT) use a padded column stride so that both
 // row and column walks by a warp are bank-conflict free.
@@ -1006,6 +1021,10 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
         const double t = rinit[i];
         if (i < m) ss[2] = fma(t, t, ss[2]); else ss[3] = fma(t, t, ss[3]);
       }
+      // the padding rows of the odd leading dimension are read by clamped
+      // (masked) loads: keep them defined
+      for (int c = tid; c < C; c += NT)
+        for (int i = R; i < ld; ++i) M[i + size_t(c) * ld] = 0.f;
       block_sum(ss, red, scal + S_RED0);
       if (tid == 0) {
         scal[S_NA] = sqrt(scal[S_RED0]);
@@ -1056,6 +1075,9 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
         }
     }
     __syncthreads();
+    dump_f(pid, 0, M, ld * C, tid);
+    dump_f(pid, 80000, tau2, RMAX, tid);
+    dump_f(pid, 80400, TQ, Ly.nbq * TSZ, tid);
     stamp(2);
 
     // ------------------------------------------ QR of C = M[0:m, 0:n], layout A
@@ -1105,6 +1127,10 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     }
   }
   __syncthreads();
+  dump_f(pid, 40000, M, ld * C, tid);
+  dump_f(pid, 84000, tau1, CMAX, tid);
+  dump_f(pid, 84200, TZ, Ly.nbz * TSZ, tid);
+  dump_f(pid, 89000, TQ, Ly.nbq * TSZ, tid);
   lap(0);
   if (iflag[0]) goto finish;
   stamp(4);
@@ -1225,7 +1251,11 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       for (int j = tid; j < n; j += NT) gf[j] = float(cout[j] / sg);
       __syncthreads();
       if (w < QG) {
-        q_apply_mw<float>(M, ld, p, m, n - p, n, TQ, false, gf, partQf, wscf, Grp{w, QG, l, 2});  // Q g
+        const Grp g{w, QG, l, 2};
+        q_apply_mw<float>(M, ld, p, m, n - p, n, TQ, false, gf, partQf, wscf, g);  // Q g
+        // the last block's updates of gf are spread over the group's warps:
+        // all of them must land before warp 0's solve reads gf(n-p:n)
+        g.sync();
         if (w == 0) trsv_upt<float>(M, ld, m, n - p, p, rinvRf, gf + (n - p), l);
       }
       __syncthreads();
@@ -1234,6 +1264,8 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       __syncthreads();
     }
   }
+  dump_d(pid, 92000, su, C, tid);
+  dump_d(pid, 92400, sw, R, tid);
   lap(1);
   stamp(5);
 
@@ -1298,6 +1330,10 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
       }
       for (int j = tid; j < n; j += NT) cout[j] = cpart[j] + cpart[CMAX + j];
       __syncthreads();
+      if (pass == 1) {
+        dump_d(pid, 93200, rout, R, tid);
+        dump_d(pid, 94000, cout, C, tid);
+      }
       if (pass == 1) stamp(6);
 
       // ---- norms, history, stop test, divergence (lse.hpp:382-396)
@@ -1509,6 +1545,13 @@ void* probe_buffer() {
 #else
   return nullptr;
 #endif
+}
+
+// debug dumps (see g_dump); returns floats per problem, DUMP_NP problems
+extern "C" int mlsb_debug_set_dump(void* buf) {
+  float* p = static_cast<float*>(buf);
+  cudaMemcpyToSymbol(reg::g_dump, &p, sizeof(p));
+  return reg::DUMP_STRIDE;
 }
 
 bool lse_reg_supported(int64_t m, int64_t n, int64_t p, int u_f, int u_s, int u_r,

@@ -282,3 +282,26 @@ def test_pipelined_host_batch_matches_device(gpu, kind):
         a, h = getattr(dev, f), getattr(host, f)
         a = a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
         assert np.array_equal(a, np.asarray(h)), f
+
+
+@pytest.mark.parametrize("shape", [(256, 128, 32), (200, 100, 50), (20, 10, 4)])
+def test_batched_bitwise_reproducible(gpu, shape):
+    """Appendix A.11: repeated launches, a sub-batch of the same problems and
+    the host-buffer path give bitwise the same results (this caught a missing
+    warp-group barrier in the register kernel's solve_v)."""
+    import torch
+
+    P = gpu
+    nb = 3000
+    A, B, b, d, _ = G.lse_batch_torch(nb, *shape, seed=1000, device="cuda")
+    o1 = P.mplse_batched(A, B, b, d)
+    o2 = P.mplse_batched(A, B, b, d)
+    sub = P.mplse_batched(A[1234:], B[1234:], b[1234:], d[1234:])
+    torch.cuda.synchronize()
+    for f in ("x", "r", "v", "iterations", "status"):
+        a1 = getattr(o1, f).cpu().numpy()
+        assert np.array_equal(a1, getattr(o2, f).cpu().numpy()), f
+        assert np.array_equal(a1[1234:], getattr(sub, f).cpu().numpy()), f
+    if shape == (256, 128, 32):
+        h = P.mplse_batched(A.cpu().numpy(), B.cpu().numpy(), b.cpu().numpy(), d.cpu().numpy())
+        assert np.array_equal(h.x, o1.x.cpu().numpy())

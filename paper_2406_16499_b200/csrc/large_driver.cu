@@ -25,6 +25,7 @@
 #include "large_common.cuh"
 #include "large_internal.h"
 #include "large_kernels.cuh"
+#include "large_cascade.cuh"
 #include "../../include/mixedls_b200.h"
 #include "mlsb_internal.h"
 
@@ -255,11 +256,119 @@ struct Blk {
 template <class FT>
 struct Fac {
   std::vector<Blk<FT>> b;
+  std::vector<BlkD<FT>> hd;  // descriptors of the persistent apply (device copy in `dev`)
+  BlkD<FT>* dev = nullptr;
+  int nrows = 0;             // max(voff + L)
 };
+
+// Scratch of the persistent cascade kernels (large_cascade.cuh), set by solve()
+// for its thread: step counters / flags and the per-step partials.
+// Three lanes, so that three streams can run persistent kernels at once (the
+// correction's independent applies and solves); `lane` selects the one the
+// next apply_F / trsv call uses.
+constexpr int CZ_LANES = 3;
+struct CzScratch {
+  static inline thread_local int* cnt = nullptr;    // per lane: [CZ_CNT] apply counters | [CZ_CNT] trsv flags
+  static inline thread_local char* part = nullptr;  // per lane: partials of k_fac_apply
+  static inline thread_local size_t part_bytes = 0; // per lane
+  static inline thread_local int lane = 0;
+  static int* lane_cnt() { return cnt ? cnt + size_t(lane) * 2 * 1024 : nullptr; }
+  static void* lane_part() { return part ? part + size_t(lane) * part_bytes : nullptr; }
+};
+constexpr int CZ_CNT = 1024;
+struct CzScratchGuard {
+  CzScratchGuard(int* c, char* p, size_t n) {
+    CzScratch::cnt = c;
+    CzScratch::part = p;
+    CzScratch::part_bytes = n;
+    CzScratch::lane = 0;
+  }
+  ~CzScratchGuard() {
+    CzScratch::cnt = nullptr;
+    CzScratch::part = nullptr;
+    CzScratch::part_bytes = 0;
+    CzScratch::lane = 0;
+  }
+};
+struct CzLane {  // RAII: apply_F / trsv calls in this scope use lane `l`
+  int prev;
+  explicit CzLane(int l) : prev(CzScratch::lane) { CzScratch::lane = l; }
+  ~CzLane() { CzScratch::lane = prev; }
+};
+// MLSB_CASCADE_OLD=1: round-1 block-per-launch applies and TRSVs (A/B switch)
+static bool cascade_on() {
+  static const bool off = getenv("MLSB_CASCADE_OLD") != nullptr;
+  return !off;
+}
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 1;
+  }
+  return n;
+}
+
+// device copy of a factor's block descriptors (after its stage is built)
+template <class FT>
+static cudaError_t fac_upload(Fac<FT>& F, BlkD<FT>* dst, cudaStream_t st) {
+  F.hd.clear();
+  F.nrows = 0;
+  for (const Blk<FT>& b : F.b) {
+    F.hd.push_back(BlkD<FT>{b.V, b.T, b.ldv, b.L, b.nbk, b.voff, b.ldt});
+    F.nrows = std::max(F.nrows, b.voff + b.L);
+  }
+  if (F.hd.empty() || int(F.hd.size()) > CZ_MAXB || !dst) return cudaSuccess;
+  F.dev = dst;
+  return cudaMemcpyAsync(dst, F.hd.data(), sizeof(BlkD<FT>) * F.hd.size(), cudaMemcpyHostToDevice, st);
+}
+
+// the whole factor in one cooperative launch; false if it does not apply
+template <class FT, class CT>
+static bool apply_F_persistent(const Fac<FT>& F, bool herm, CT* x, cudaStream_t st) {
+  if (!cascade_on() || !F.dev || !CzScratch::cnt) return false;
+  constexpr int RB = 32 * (16 / sizeof(FT) > 0 ? 16 / sizeof(FT) : 1);
+  const int nb = int(F.hd.size());
+  const int G = (F.nrows + RB - 1) / RB;
+  if (nb == 0 || G > sm_count() ||
+      size_t(nb) * G * 128 * sizeof(CT) > CzScratch::part_bytes || nb > CZ_CNT)
+    return false;
+  int* cnt = CzScratch::lane_cnt();
+  if (cudaMemsetAsync(cnt, 0, sizeof(int) * nb, st) != cudaSuccess) return false;
+  const BlkD<FT>* blks = F.dev;
+  int hm = herm ? 1 : 0, nr = F.nrows;
+  CT* part = static_cast<CT*>(CzScratch::lane_part());
+  const size_t sm = sizeof(FT) * 128 * (128 + 16 / sizeof(FT));  // staged T_b
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_fac_apply<FT, CT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) ||
+        cudaFuncSetAttribute(k_fac_apply<FT, CT, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) ||
+        cudaFuncSetAttribute(k_fac_apply<FT, CT, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) ||
+        cudaFuncSetAttribute(k_fac_apply<FT, CT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)))
+      return false;
+    attr = true;
+  }
+  (void)hm;
+  // 16-byte loads when every block's columns start 16-byte aligned at every
+  // CTA's first row (voff, ldv and the base multiples of the vector width)
+  bool al = true;
+  for (const BlkD<FT>& b : F.hd)
+    al = al && (reinterpret_cast<uintptr_t>(b.V) % 16 == 0) && (b.ldv * sizeof(FT)) % 16 == 0 &&
+         (size_t(b.voff) * sizeof(FT)) % 16 == 0;
+  void* args[] = {(void*)&blks, (void*)&nb, (void*)&x, (void*)&nr, (void*)&part, (void*)&cnt};
+  void* fn = herm ? (al ? reinterpret_cast<void*>(k_fac_apply<FT, CT, true, true>)
+                        : reinterpret_cast<void*>(k_fac_apply<FT, CT, true, false>))
+                  : (al ? reinterpret_cast<void*>(k_fac_apply<FT, CT, false, true>)
+                        : reinterpret_cast<void*>(k_fac_apply<FT, CT, false, false>));
+  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(CZ_NT), args, sm, st) == cudaSuccess;
+}
 
 // ypart: WYB * 256 partials of the dot kernel
 template <class FT, class CT>
 static void apply_F(const Fac<FT>& F, bool herm, CT* x, CT* ypart, cudaStream_t st) {
+  if (apply_F_persistent<FT, CT>(F, herm, x, st)) return;
   const int nb = int(F.b.size());
   for (int s = 0; s < nb; ++s) {
     const Blk<FT>& b = F.b[herm ? s : nb - 1 - s];
@@ -275,8 +384,31 @@ static void apply_F(const Fac<FT>& F, bool herm, CT* x, CT* ypart, cudaStream_t 
 // upper-triangular solve with U = M[r0:r0+k, c0:c0+k]; herm: U^H x = b.
 // Diagonal blocks of TRB = 128 (one CTA each), off-diagonal GEMV updates.
 template <class FT, class CT>
+static bool trsv_persistent(const FT* M, int64_t ld, int64_t r0, int64_t c0, int k, bool herm, CT* x,
+                            cudaStream_t st) {
+  if (!cascade_on() || !CzScratch::cnt || k <= 0) return false;
+  const int K = (k + CZT - 1) / CZT;
+  if (K > sm_count() || K > CZ_CNT) return false;
+  const size_t sm = sizeof(FT) * CZT * (CZT + 1) + sizeof(CT) * CZT * 6;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_trsv_chain<FT, CT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) ||
+        cudaFuncSetAttribute(k_trsv_chain<FT, CT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)))
+      return false;
+    attr = true;
+  }
+  int* flags = CzScratch::lane_cnt() + CZ_CNT;
+  if (cudaMemsetAsync(flags, 0, sizeof(int) * K, st) != cudaSuccess) return false;
+  void* args[] = {(void*)&M, (void*)&ld, (void*)&r0, (void*)&c0, (void*)&k, (void*)&x, (void*)&flags};
+  void* fn = herm ? reinterpret_cast<void*>(k_trsv_chain<FT, CT, true>)
+                  : reinterpret_cast<void*>(k_trsv_chain<FT, CT, false>);
+  return cudaLaunchCooperativeKernel(fn, dim3(K), dim3(CZ_NT), args, sm, st) == cudaSuccess;
+}
+
+template <class FT, class CT>
 static void trsv(const FT* M, int64_t ld, int64_t r0, int64_t c0, int k, bool herm, CT* x,
                  cudaStream_t st) {
+  if (trsv_persistent<FT, CT>(M, ld, r0, c0, k, herm, x, st)) return;
   const size_t sm = sizeof(FT) * TRB * (TRB + 1) + sizeof(CT) * TRB;
   static bool attr = false;
   if (!attr) {
@@ -1167,6 +1299,12 @@ static int gmres_correction_gls(int kind, int n, int m, int p, double alpha, con
   return MLSB_OK;
 }
 
+// debug: CTA-0 globaltimer stamps of the persistent apply (8 per block)
+extern "C" int mlsb_debug_set_czstamps(void* buf) {
+  unsigned long long* p = static_cast<unsigned long long*>(buf);
+  return int(cudaMemcpyToSymbol(g_czstamp, &p, sizeof(p)));
+}
+
 // --------------------------------------------------------------- driver
 template <class FT, class WT, class CT>
 static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
@@ -1192,6 +1330,11 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   const bool lows = P.u_s == 0;  // correction at u_s = low: one demotion scale (refine.hpp:103-119)
   const bool lowf = P.u_f == 0;  // pre-scaling only at u_f = low (lse.hpp:315-318, gls.hpp:287-289)
 
+  // persistent cascade scratch: 2 x CZ_CNT ints, 2 x CZ_MAXB descriptors, and
+  // the per-step partials of k_fac_apply (steps x CTAs x 128, the widest CT)
+  const size_t cz_part = size_t(std::max(obz, obq)) * 160 * 128 * sizeof(cd);
+  const size_t cz_bytes =
+      CZ_LANES * (2 * CZ_CNT * sizeof(int) + cz_part + 256) + 2 * CZ_MAXB * sizeof(BlkD<FT>) + 1024;
   Arena ar;
   const size_t bytes = sizeof(FT) * (size_t(R) * C + size_t(obz) * R * NBO + size_t(obq) * C * NBO +
                                      size_t(nbz + nbq) * NB * NB + size_t(C + R) + 2 * size_t(L) * NBO +
@@ -1200,7 +1343,8 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
                        sizeof(WT) * (size_t(R) * (6 + ntc) + size_t(C) * (5 + ntr)) +
                        (ext ? 16 * (size_t(ntc) * R + size_t(ntr) * C) + 8 * size_t(R) : 0) +
                        sizeof(CT) * (10 * size_t(L) + WYB * 256 + WYB + 4) +
-                       (sizeof(CT) + sizeof(FT)) * size_t(L) * ((L + GNC - 1) / GNC) + 64 * 1024 + 64 * 256;
+                       (sizeof(CT) + sizeof(FT)) * size_t(L) * ((L + GNC - 1) / GNC) + 64 * 1024 + 64 * 256 +
+                       cz_bytes;
   cudaError_t e = ar.init(bytes + bytes / 4 + (1 << 20), st);
   if (e) return MLSB_ERR_CUDA;
   FT* M = ar.take<FT>(size_t(R) * C);
@@ -1252,6 +1396,11 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   StopOut* so = reinterpret_cast<StopOut*>(small + 34 * 1024);
   cudaMemsetAsync(small, 0, 64 * 1024, st);
   cudaMemsetAsync(ypart, 0, sizeof(CT) * (WYB * 256 + WYB + 4), st);  // apply tickets start at 0
+  int* cz_cnt = ar.take<int>(CZ_LANES * 2 * CZ_CNT);
+  BlkD<FT>* cz_desc = ar.take<BlkD<FT>>(2 * CZ_MAXB);
+  char* cz_p = ar.take<char>(CZ_LANES * cz_part);
+  if (!cz_p) return MLSB_ERR_CUDA;
+  CzScratchGuard czg(cz_cnt, cz_p, cz_part);
   GemvScratchGuard<CT> gsg_c(gscr, gsn);
   std::unique_ptr<GemvScratchGuard<FT>> gsg_f;
   if constexpr (!std::is_same<FT, CT>::value) gsg_f.reset(new GemvScratchGuard<FT>(gscr_f, gsn));
@@ -1373,6 +1522,33 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   } else {
     if ((e = qr_stage<FT>(M, ld, n, kz, m + p, VZ, TZ, TZb, tauZ, FZ, SS))) return MLSB_ERR_CUDA;
     if ((e = rq_stage<FT>(M, ld, 0, n, m, p, VQ, TQ, TQb, tauQ, FQ, SS))) return MLSB_ERR_CUDA;
+  }
+  if ((e = fac_upload<FT>(FZ, cz_desc, st)) || (e = fac_upload<FT>(FQ, cz_desc + CZ_MAXB, st)))
+    return MLSB_ERR_CUDA;
+  // the correction's independent applies / solves on three streams, when every
+  // piece runs as a persistent launch (each lane owns its scratch)
+  const int vec_rows = 32 * int(16 / sizeof(FT) > 0 ? 16 / sizeof(FT) : 1);
+  const bool par = cascade_on() && FZ.dev && FQ.dev && int(FZ.hd.size()) <= CZ_CNT &&
+                   int(FQ.hd.size()) <= CZ_CNT && (FZ.nrows + vec_rows - 1) / vec_rows <= sm_count() &&
+                   (FQ.nrows + vec_rows - 1) / vec_rows <= sm_count() &&
+                   (std::max({m, n, p}) + CZT - 1) / CZT <= sm_count() && !getenv("MLSB_CASCADE_SERIAL");
+  cudaStream_t cs2 = nullptr, cs3 = nullptr;
+  cudaEvent_t cev[6] = {};
+  struct CzStreams {
+    cudaStream_t& a;
+    cudaStream_t& b;
+    cudaEvent_t* ev;
+    ~CzStreams() {
+      if (a) cudaStreamDestroy(a);
+      if (b) cudaStreamDestroy(b);
+      for (int i = 0; i < 6; ++i)
+        if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+  } czs_guard{cs2, cs3, cev};
+  if (par) {
+    cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&cs3, cudaStreamNonBlocking);
+    for (int i = 0; i < 6; ++i) cudaEventCreateWithFlags(&cev[i], cudaEventDisableTiming);
   }
   // zero pivots in the order of the reference's first failing trsv
   // (LSE: R at lse.hpp:53, then T11 at :60; GLS: T22 at gls.hpp:55, then R at :61)
@@ -1669,7 +1845,65 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
     }
     // ---- correction at u_s (demotion by one sigma, refine.hpp:103-107)
     const unsigned long long* sb = lows ? bits + 5 : nullptr;
-    if (lse) {  // Algorithm 1 (lse.hpp:83-128)
+    if (lse && par) {  // Algorithm 1 (lse.hpp:83-128), independent pieces on three streams
+      const int k = kl;
+      CT *u = cv[0], *w = cv[1], *y2 = cv[2], *q1 = cv[3], *t4 = cv[4], *y = cv[5], *dr = cv[6],
+         *tq = cv[7];
+      k_demote<WT, CT><<<nblk(n), KT, 0, st>>>(cout, n, sb, u);
+      k_demote<WT, CT><<<nblk(m), KT, 0, st>>>(rout, m, sb, w);
+      k_demote<WT, CT><<<nblk(p), KT, 0, st>>>(rout + m, p, sb, y2);
+      mark("demote");
+      cudaEventRecord(cev[0], st);
+      cudaStreamWaitEvent(cs2, cev[0], 0);
+      cudaStreamWaitEvent(cs3, cev[0], 0);
+      {
+        CzLane ln(1);
+        apply_F<FT, CT>(FQ, true, u, ypart, cs2);                 // u = Q f3 = F^H f3
+        k_copy<CT><<<nblk(k), KT, 0, cs2>>>(u, k, q1);
+        trsv<FT, CT>(M, ld, 0, 0, k, true, q1, cs2);              // T11^H q1 = u1
+      }
+      {
+        CzLane ln(2);
+        trsv<FT, CT>(M, ld, m, n - p, p, false, y2, cs3);         // R y2 = f2
+        gemv_n<FT, CT>(M, ld, 0, k, k, p, none, y2, t4, cs3);      // T12 y2
+        gemv_n<FT, CT>(M, ld, k, m - k, k, p, Mask{1, 0, 0}, y2, t4 + k, cs3);  // T22 y2
+      }
+      apply_F<FT, CT>(FZ, true, w, ypart, st);                    // w = Z^H f1
+      cudaEventRecord(cev[1], cs2);
+      cudaEventRecord(cev[2], cs3);
+      cudaStreamWaitEvent(st, cev[1], 0);
+      cudaStreamWaitEvent(st, cev[2], 0);
+      mark("phaseA");
+      k_subsub<CT><<<nblk(k), KT, 0, st>>>(w, q1, t4, k, y);      // y1 rhs = w1 - q1 - T12 y2
+      k_copy<CT><<<nblk(k), KT, 0, st>>>(q1, k, w);               // q = [q1; w2 - T22 y2]
+      k_sub<CT><<<nblk(m - k), KT, 0, st>>>(w + k, t4 + k, m - k, w + k);
+      k_copy<CT><<<nblk(m), KT, 0, st>>>(w, m, dr);
+      k_copy<CT><<<nblk(p), KT, 0, st>>>(y2, p, y + k);
+      cudaEventRecord(cev[3], st);
+      cudaStreamWaitEvent(cs2, cev[3], 0);
+      cudaStreamWaitEvent(cs3, cev[3], 0);
+      {
+        CzLane ln(1);
+        apply_F<FT, CT>(FZ, false, dr, ypart, cs2);               // dr = Z q = F q
+      }
+      {
+        CzLane ln(2);
+        gemv_h<FT, CT>(M, ld, 0, k, k, p, none, w, t4, cs3);       // T12^H q1
+        gemv_h<FT, CT>(M, ld, k, m - k, k, p, Mask{1, 0, 0}, w + k, tq, cs3);  // T22^H q2
+        k_addsub<CT><<<nblk(p), KT, 0, cs3>>>(t4, tq, u + k, p, t4);  // s = T12^H q1 + (T22^H q2 - u2)
+        trsv<FT, CT>(M, ld, m, n - p, p, true, t4, cs3);           // R^H dv = s
+      }
+      trsv<FT, CT>(M, ld, 0, 0, k, false, y, st);                 // T11 y1 = ...
+      apply_F<FT, CT>(FQ, false, y, ypart, st);                   // dx = Q^H y = F y
+      cudaEventRecord(cev[4], cs2);
+      cudaEventRecord(cev[5], cs3);
+      cudaStreamWaitEvent(st, cev[4], 0);
+      cudaStreamWaitEvent(st, cev[5], 0);
+      mark("phaseB");
+      k_promote_add<WT, CT><<<nblk(m), KT, 0, st>>>(sw, m, dr, sb, false, flags + 3);
+      k_promote_add<WT, CT><<<nblk(p), KT, 0, st>>>(sw + m, p, t4, sb, false, flags + 3);
+      k_promote_add<WT, CT><<<nblk(n), KT, 0, st>>>(su, n, y, sb, false, flags + 3);
+    } else if (lse) {  // Algorithm 1 (lse.hpp:83-128)
       const int k = kl;
       CT *u = cv[0], *w = cv[1], *y2 = cv[2], *q1 = cv[3], *t4 = cv[4], *y = cv[5], *dr = cv[6],
          *tq = cv[7];
@@ -1710,6 +1944,67 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       k_promote_add<WT, CT><<<nblk(m), KT, 0, st>>>(sw, m, dr, sb, false, flags + 3);
       k_promote_add<WT, CT><<<nblk(p), KT, 0, st>>>(sw + m, p, t4, sb, false, flags + 3);
       k_promote_add<WT, CT><<<nblk(n), KT, 0, st>>>(su, n, y, sb, false, flags + 3);
+    } else if (par) {  // Algorithm 3 (gls.hpp:106-154), independent pieces on three streams
+      const int nm = n - m, kp = kl;
+      const int kk = std::min(n, p);
+      const Mask rqm{2, n - kk, m + (p - kk)};
+      CT *u = cv[0], *w = cv[1], *h1 = cv[2], *g2 = cv[3], *t4 = cv[4], *r2 = cv[5], *g = cv[6],
+         *r1v = cv[7], *tq = cv[8], *hh = cv[9];
+      k_demote<WT, CT><<<nblk(n), KT, 0, st>>>(rout, n, sb, u);       // f2
+      k_demote<WT, CT><<<nblk(p), KT, 0, st>>>(cout + m, p, sb, w);   // f1
+      k_demote<WT, CT><<<nblk(m), KT, 0, st>>>(cout, m, sb, h1);      // f3
+      mark("demote");
+      cudaEventRecord(cev[0], st);
+      cudaStreamWaitEvent(cs2, cev[0], 0);
+      cudaStreamWaitEvent(cs3, cev[0], 0);
+      {
+        CzLane ln(1);
+        apply_F<FT, CT>(FZ, true, u, ypart, cs2);                       // u = Q^H f2
+        k_copy<CT><<<nblk(nm), KT, 0, cs2>>>(u + m, nm, g2);
+        trsv<FT, CT>(M, ld, m, m + kp, nm, false, g2, cs2);             // T22 g2 = u2
+      }
+      {
+        CzLane ln(2);
+        trsv<FT, CT>(M, ld, 0, 0, m, true, h1, cs3);                    // R^H h1 = f3
+        gemv_h<FT, CT>(M, ld, 0, m, m + kp, nm, none, h1, t4, cs3);      // T12^H h1
+        gemv_h<FT, CT>(M, ld, 0, m, m, kp, rqm, h1, tq, cs3);            // T11^H h1
+      }
+      apply_F<FT, CT>(FQ, true, w, ypart, st);                          // w = Z f1 = F^H f1
+      cudaEventRecord(cev[1], cs2);
+      cudaEventRecord(cev[2], cs3);
+      cudaStreamWaitEvent(st, cev[1], 0);
+      cudaStreamWaitEvent(st, cev[2], 0);
+      mark("phaseA");
+      k_subsub<CT><<<nblk(nm), KT, 0, st>>>(w + kp, g2, t4, nm, r2);  // w2 - g2 - T12^H h1
+      k_sub<CT><<<nblk(kp), KT, 0, st>>>(w, tq, kp, g);               // g1 = w1 - T11^H h1
+      k_copy<CT><<<nblk(nm), KT, 0, st>>>(g2, nm, g + kp);
+      k_copy<CT><<<nblk(p), KT, 0, st>>>(g, p, hh);
+      cudaEventRecord(cev[3], st);
+      cudaStreamWaitEvent(cs2, cev[3], 0);
+      cudaStreamWaitEvent(cs3, cev[3], 0);
+      {
+        CzLane ln(1);
+        apply_F<FT, CT>(FQ, false, hh, ypart, cs2);                     // dy = Z^H g = F g
+      }
+      {
+        CzLane ln(2);
+        gemv_n<FT, CT>(M, ld, 0, m, m, kp, rqm, g, t4, cs3);             // T11 g1
+        gemv_n<FT, CT>(M, ld, 0, m, m + kp, nm, none, g2, tq, cs3);      // T12 g2
+        k_sub2<CT><<<nblk(m), KT, 0, cs3>>>(u, t4, tq, m, r1v);        // u1 - (T11 g1 + T12 g2)
+        trsv<FT, CT>(M, ld, 0, 0, m, false, r1v, cs3);                  // R dx = ...
+      }
+      trsv<FT, CT>(M, ld, m, m + kp, nm, true, r2, st);                 // T22^H h2 = ...
+      k_copy<CT><<<nblk(m), KT, 0, st>>>(h1, m, u);
+      k_copy<CT><<<nblk(nm), KT, 0, st>>>(r2, nm, u + m);
+      apply_F<FT, CT>(FZ, false, u, ypart, st);                          // Q [h1; h2]
+      cudaEventRecord(cev[4], cs2);
+      cudaEventRecord(cev[5], cs3);
+      cudaStreamWaitEvent(st, cev[4], 0);
+      cudaStreamWaitEvent(st, cev[5], 0);
+      mark("phaseB");
+      k_promote_add<WT, CT><<<nblk(m), KT, 0, st>>>(su, m, r1v, sb, false, flags + 3);
+      k_promote_add<WT, CT><<<nblk(p), KT, 0, st>>>(su + m, p, hh, sb, false, flags + 3);
+      k_promote_add<WT, CT><<<nblk(n), KT, 0, st>>>(sw, n, u, sb, true, flags + 3);  // dz = -Q h
     } else {    // Algorithm 3 (gls.hpp:106-154)
       const int nm = n - m, kp = kl;
       const int kk = std::min(n, p);

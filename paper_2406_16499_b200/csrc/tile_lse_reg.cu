@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "device_common.cuh"
 #include "mlsb_internal.h"
@@ -1521,12 +1522,15 @@ finish:
 template <class CT>
 static cudaError_t launch_ct(const TileArgs& a, cudaStream_t st) {
   const Layout L = make_layout(a.m, a.n, a.p, sizeof(CT));
+  static const int opts = getenv("MLSB_REG_OPTS") ? atoi(getenv("MLSB_REG_OPTS")) : 0;
+  TileArgs a2 = a;
+  a2.opts = opts;
   auto kern = (a.m == 256 && a.n == 128 && a.p == 32) ? lse_reg_kernel<CT, 256, 128, 32>
                                                       : lse_reg_kernel<CT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(L.total));
   if (e != cudaSuccess) return e;
-  kern<<<dim3(unsigned(a.batch)), dim3(NT), L.total, st>>>(a);
+  kern<<<dim3(unsigned(a.batch)), dim3(NT), L.total, st>>>(a2);
   return cudaGetLastError();
 }
 

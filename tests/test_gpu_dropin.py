@@ -42,3 +42,41 @@ def test_dropin_demo_exception_path_without_gpu():
     r = subprocess.run([DEMO], capture_output=True, text=True, timeout=120)
     # the first GPU call raises mixedls::error (no device) -> non-zero exit
     assert r.returncode != 0
+
+
+HARN_GPU = os.path.join(ROOT, "oracle", "_ref", "b200_harness")
+HARN_REF = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
+CELL = re.compile(r"CELL (\d+) kind (\w+) cond (\S+) method (\S+) status (\w+) iters (\d+) inner (\d+) m1 (\S+) m2 (\S+)")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["lse", "gls"])
+def test_reference_run_sweep_routed_to_b200(gpu, kind):
+    """The reference's own run_experiment / run_sweep (unmodified
+    inc/experiment.hpp, desk-scale paper_sweep_cells) with its IR and GMRES-IR
+    calls routed to the B200 library (tests/harness_b200.cpp), against the same
+    sweep on the plain reference: same status per cell, outer passes within 1,
+    err-1 / err-2 (er-1 / er-2) of converged cells within 10x."""
+    if not (os.path.exists(HARN_GPU) and os.path.exists(HARN_REF)):
+        pytest.skip("harness not built (needs /root/reference at build time)")
+    env = dict(os.environ, MIXEDLS_THREADS="1")  # one GPU: cells in order
+    g = subprocess.run([HARN_GPU, kind], capture_output=True, text=True, timeout=600, env=env)
+    r = subprocess.run([HARN_REF, kind], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, MIXEDLS_THREADS=str(os.cpu_count() or 1)))
+    assert g.returncode == 0 and r.returncode == 0, (g.stderr, r.stderr)
+    gc, rc = CELL.findall(g.stdout), CELL.findall(r.stdout)
+    assert len(gc) == len(rc) > 0, (g.stdout, r.stdout)
+    bad = []
+    for a, b in zip(gc, rc):
+        if a[:4] != b[:4]:
+            bad.append(("cell mismatch", a, b))
+            continue
+        st_g, st_r, it_g, it_r = a[4], b[4], int(a[5]), int(b[5])
+        if st_g != st_r or abs(it_g - it_r) > 1:
+            bad.append((a, b))
+            continue
+        if st_g == "converged":
+            for k in (7, 8):
+                if not float(a[k]) <= max(10 * float(b[k]), 1e-12):
+                    bad.append(("metric", k, a, b))
+    assert not bad, bad

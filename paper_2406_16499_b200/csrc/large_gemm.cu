@@ -327,8 +327,34 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
     __syncthreads();
     buf ^= 1;
   }
-  // epilogue: column by column, 4-row groups (float4 when aligned)
+  // epilogue: column by column, 4-row groups (float4 when aligned).  In the
+  // vector path the C reads of a row half are all issued before its first
+  // store: C's loads and stores may alias, so interleaved they would each pay
+  // a full memory latency.
   const bool cvec = VEC && ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && (ldc & 3) == 0 && (i0 & 3) == 0;
+  if (cvec && i0 + 128 <= M && j0 + 128 <= N) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gi = i0 + h * 64 + tr * 4;
+      float4 o[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int gj = j0 + (b < 4 ? tc * 4 + b : 64 + tc * 4 + b - 4);
+        o[b] = beta != 0.f ? *reinterpret_cast<const float4*>(C + int64_t(gj) * ldc + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int gj = j0 + (b < 4 ? tc * 4 + b : 64 + tc * 4 + b - 4);
+        float4 v = make_float4(alpha * acc[4 * h][b], alpha * acc[4 * h + 1][b], alpha * acc[4 * h + 2][b],
+                               alpha * acc[4 * h + 3][b]);
+        if (beta != 0.f)
+          v.x = fmaf(beta, o[b].x, v.x), v.y = fmaf(beta, o[b].y, v.y), v.z = fmaf(beta, o[b].z, v.z),
+          v.w = fmaf(beta, o[b].w, v.w);
+        *reinterpret_cast<float4*>(C + int64_t(gj) * ldc + gi) = v;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
     const int gj = j0 + (b < 4 ? tc * 4 + b : 64 + tc * 4 + b - 4);
@@ -494,8 +520,11 @@ static void launch128(bool ha, bool hb, dim3 tiles, int M, int N, int K, float a
   const int nt = int(tiles.x * tiles.y * tiles.z);
   const int grid = g_gemm_cta_cap > 0 ? std::min(nt, g_gemm_cta_cap) : nt;
   const int gm = int(tiles.x), gn = int(tiles.y), gz = int(tiles.z);
+  // k-tile per operand layout: the NT form (B transposed, the RQ trailing
+  // update) spills at BK = 32 and is fastest at 16; the others at 32
+  // (scripts/dbg/gemm_rate.py at the C3 shapes)
   static const bool bk16 = getenv("MLSB_GEMM_BK16") != nullptr;
-  if (bk16)
+  if (bk16 || (!ha && hb))
     launch128_bk<VEC, 16>(ha, hb, grid, gm, gn, gz, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, st);
   else
     launch128_bk<VEC, GBK>(ha, hb, grid, gm, gn, gz, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, st);

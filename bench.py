@@ -298,7 +298,9 @@ def c4_parity(A, B, b, d, kA, out, ref):
     fwd_bad = ~(fwd <= bound)
     idiff = np.abs(it_g.astype(np.int64) - it_r.astype(np.int64))
     fr = (fwd / bound).cpu().numpy()
-    return {"c4_checked": int(A.shape[0]), "against": "oracle/_ref (unmodified reference)",
+    ok = (int(idiff.max()) <= 1 and int((st_g != st_r).sum()) == 0 and int(fwd_bad.sum().item()) == 0
+          and int(be_bad.sum().item()) == 0)
+    return {"ok": ok, "c4_checked": int(A.shape[0]), "against": "oracle/_ref (unmodified reference)",
             "max_iter_diff": int(idiff.max()), "iter_diff_hist": {str(k): int((idiff == k).sum())
                                                                   for k in range(int(idiff.max()) + 1)},
             "mean_passes_gpu": float(it_g.mean()), "mean_passes_ref": float(it_r.mean()),

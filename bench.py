@@ -312,6 +312,12 @@ def c4_parity(A, B, b, d, kA, out, ref):
             "max_backward_gpu": float(be_g.max().item()), "max_backward_ref": float(be_r.max().item())}
 
 
+# MLSB_BENCH_DIST=gloo: the N > 1 code path on ONE GPU (all ranks on cuda:0,
+# collectives through host copies) -- a functional check of the sharded
+# bench where this sandbox has a single GPU; never used for a measurement
+DIST_BACKEND = os.environ.get("MLSB_BENCH_DIST", "nccl")
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -322,7 +328,9 @@ def run_ours(args, rank, world, local_rank):
     from paper_2406_16499_b200 import generate as G
     from paper_2406_16499_b200.dist import shard_plan
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank if DIST_BACKEND == "nccl" else 0)
+    if DIST_BACKEND != "nccl":
+        local_rank = 0
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
     total = args.batch
@@ -344,6 +352,8 @@ def run_ours(args, rank, world, local_rank):
         flat = torch.cat(parts, dim=1)
         if flat.shape[0] < width:
             flat = torch.cat([flat, flat.new_zeros((width - flat.shape[0], flat.shape[1]))])
+        if DIST_BACKEND != "nccl":
+            flat = flat.cpu()
         bufs = [torch.empty_like(flat) for _ in range(world)] if rank == 0 else None
         dist.gather(flat, bufs, dst=0)
         if rank == 0:
@@ -378,7 +388,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev if DIST_BACKEND == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -395,7 +405,8 @@ def run_ours(args, rank, world, local_rank):
         gather(out)
         g1.record(stream)
         torch.cuda.synchronize()
-        tg = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device=dev)
+        tg = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64,
+                          device=dev if DIST_BACKEND == "nccl" else "cpu")
         dist.all_reduce(tg, op=dist.ReduceOp.MAX)
         gather_ms = float(tg.item())
 
@@ -407,7 +418,8 @@ def run_ours(args, rank, world, local_rank):
               "diverged": int((status == 2).sum()), "errors": int((err != 0).sum())}
     if world > 1:
         st = torch.tensor([solves["converged"], solves["max_iterations"], solves["diverged"],
-                           solves["errors"], int(iters.sum())], dtype=torch.float64, device=dev)
+                           solves["errors"], int(iters.sum())], dtype=torch.float64,
+                          device=dev if DIST_BACKEND == "nccl" else "cpu")
         dist.all_reduce(st)
         solves = {"iterations_mean": float(st[4]) / total, "converged": int(st[0]),
                   "max_iterations": int(st[1]), "diverged": int(st[2]), "errors": int(st[3])}
@@ -484,7 +496,7 @@ def run_ours(args, rank, world, local_rank):
             e2e_step()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev if DIST_BACKEND == "nccl" else "cpu")
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
@@ -668,6 +680,7 @@ def single_records(args, peak32):
     if not args.no_c5:
         gpu["C5"] = _gpu_single(PK, "gls", inp5, cfg_of(c5), reps=3) + (gen5,)
     gemm = trailing_gemm_record(peak32)
+    gmres = gmres_records(PK, probs, c3)
     for th in threads:
         th.join()
 
@@ -718,7 +731,37 @@ def single_records(args, peak32):
             par["C5"] = {"ok": False, "oracle_error": cerr}
         recs["C5"] = rec
     recs["trailing_update_gemm"] = gemm
+    recs["gmres_ir_c3"] = gmres
     return recs, par
+
+
+def gmres_records(PK, probs, c3):
+    """GMRES-IR (gmres_refine_lse, inc/krylov.hpp:545-689) at
+    the C3 shape, both preconditioners, at kappa_A 1e4 and 1e6 (where
+    classical IR approaches its limit): device phases, outer / inner
+    iterations, wall time through the public API.  GPU only: the reference's
+    GMRES-IR at this size is minutes of CPU time (its factorization alone is
+    ~80 s); parity at size is tests/test_gpu_atsize.py."""
+    import torch
+
+    out = {}
+    for key, (inp, kap, _) in probs.items():
+        if kap not in (1e4, 1e6):
+            continue
+        for pc in ("bd_split", "left"):
+            cfg = PK.RefinementConfig(maxit=c3["maxit"])
+            PK.gmres_refine_lse(PK.LseProblem(*inp), cfg, precond=pc)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = PK.gmres_refine_lse(PK.LseProblem(*inp), cfg, precond=pc)
+            wall = time.perf_counter() - t0
+            ph = dict(r.trace.timing)
+            out[f"{key}_{pc}"] = {"status": r.trace.status, "outer": r.trace.iterations,
+                                  "inner": r.trace.inner_iterations, "device_ms": sum(ph.values()) * 1e3,
+                                  "wall_ms": wall * 1e3, "phases_ms": {q: v * 1e3 for q, v in ph.items()},
+                                  "ms_per_inner": (ph["gmres"] * 1e3 / r.trace.inner_iterations
+                                                   if r.trace.inner_iterations else None)}
+    return out
 
 
 def trailing_gemm_record(peak32):
@@ -763,7 +806,7 @@ def main():
     if world > 1:
         import torch
 
-        if args.impl == "ours":
+        if args.impl == "ours" and DIST_BACKEND == "nccl":
             torch.cuda.set_device(local_rank)
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:

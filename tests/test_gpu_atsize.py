@@ -123,3 +123,26 @@ def test_c4_full_batch_vs_reference(gpu, ref):
     assert bad.size == 0, (bad[:10], (fwd / bound)[bad[:10]])
     assert np.abs(it.astype(np.int64) - it_r).max() <= 1
     assert np.array_equal(st, st_r)
+
+
+def test_c3_gmres_ir_kappa_1e6_vs_reference(gpu, ref):
+    """GMRES-IR with the block-diagonal split preconditioner (gmres_refine_lse,
+    inc/krylov.hpp:545-689) at the C3 shape and kappa_A 1e6 -- where it is the
+    rescue for classical IR -- against the unmodified
+    reference: same status, outer passes within 1, forward error bound."""
+    P = gpu
+    c = G.CONFIGS["C3"]
+    m, n, p = c["m"], c["n"], c["p"]
+    A, B, b, d = G.lse_problem(m, n, p, 1e6, c["kappa_B"], c["seed"])
+    ths, refs = _run_threads({"g": lambda: ref.gmres_lse(A, B, b, d, maxit=c["maxit"], prec=("s", "s", "d"),
+                                                         precond="bd_split")})
+    res = P.gmres_refine_lse(P.LseProblem(A, B, b, d), P.RefinementConfig(maxit=c["maxit"]),
+                             precond="bd_split")
+    for t in ths:
+        t.join()
+    rr = refs["g"]
+    assert not isinstance(rr, Exception), rr
+    assert res.trace.status == rr.status == "converged"
+    assert abs(res.trace.iterations - rr.iterations) <= 1, (res.trace.iterations, rr.iterations)
+    assert rel(res.state.x, rr.x) <= fwd_bound(m, n, p, 1e6)
+    assert res.trace.timing["gmres"] > 0 and res.trace.timing["correction"] == 0

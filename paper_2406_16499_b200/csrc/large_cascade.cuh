@@ -337,8 +337,11 @@ template <class FT, class CT, bool HERM>
 __global__ void __launch_bounds__(CZ_NT, 1) k_trsv_chain(const FT* M, int64_t ld, int64_t r0, int64_t c0,
                                                          int k, CT* x, int* flags) {
   extern __shared__ __align__(16) unsigned char czsm_[];
-  constexpr int LU = CZT + 1;
-  FT* Ud = reinterpret_cast<FT*>(czsm_);                 // diagonal block, Ud[i + j LU]
+  constexpr int LU = CZT + 4;  // 16-byte aligned columns (4-row vector loads)
+  // diagonal block: !HERM Ud[i + j LU] = U(i, j) (upper); HERM Ud[i + j LU] =
+  // conj(U(j, i)) (the lower triangle of U^H), so both solves read a column of
+  // four consecutive rows per lane
+  FT* Ud = reinterpret_cast<FT*>(czsm_);
   CT* xs = reinterpret_cast<CT*>(Ud + CZT * LU);        // b_j, then x_j
   CT* xi = xs + CZT;                                     // a solved block x_i
   CT* red = xi + CZT;                                    // [4][CZT] partials
@@ -357,7 +360,10 @@ __global__ void __launch_bounds__(CZ_NT, 1) k_trsv_chain(const FT* M, int64_t ld
       t[u] = (rr <= jj && jj < bs) ? mp[int64_t(4 * u) * ld] : zero<FT>();
     }
 #pragma unroll
-    for (int u = 0; u < 32; ++u) Ud[rr + (h + 4 * u) * LU] = t[u];
+    for (int u = 0; u < 32; ++u) {
+      if (!HERM) Ud[rr + (h + 4 * u) * LU] = t[u];
+      else Ud[(h + 4 * u) + rr * LU] = conj_(t[u]);
+    }
   }
   if (tid < CZT) xs[tid] = tid < bs ? x[i0 + tid] : zero<CT>();
 
@@ -435,70 +441,100 @@ __global__ void __launch_bounds__(CZ_NT, 1) k_trsv_chain(const FT* M, int64_t ld
   }
 
   czstamp_any(4 * j + 1);
-  // diagonal block: ONE warp, lane l owns rows l + 32 t (t < 4) in registers;
-  // step j: every lane forms its quotient, the owner's is broadcast, every lane
-  // updates its rows still below (!HERM: above) the pivot.  No CTA barrier on
-  // the 128-step chain; the U entries of a step come from shared memory
-  // (conflict-free: consecutive rows of a column / columns of a row at an odd
-  // stride) and do not depend on the chain, so they issue ahead.
+  // diagonal block: ONE warp; lane l owns the four consecutive rows 4l .. 4l+3
+  // in registers.  Group g (rows 4g .. 4g+3, last to first for U, first to
+  // last for U^H): lane g solves its 4 x 4 triangle serially in registers,
+  // broadcasts the four values, every lane still to update subtracts their
+  // column block from its rows.  The chain per four rows is one 4 x 4 solve
+  // plus four shuffles (round 1 / earlier round 2: one shuffle per row); the
+  // 16 coupling entries of the next group are loaded while the current one
+  // runs (conflict-free 16-byte loads of four consecutive rows).
   if (w == 0) {
-    CT xv[4], pv[4], rp[4];
+    CT xv[4];
+    const int rq0 = 4 * l;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int rw = l + 32 * t;
-      const bool lin = rw < bs;
-      xv[t] = lin ? xs[rw] : zero<CT>();
-      const CT pd = widen_to<CT>(Ud[(lin ? rw : 0) * (LU + 1)]);
-      pv[t] = lin ? (HERM ? conj_(pd) : pd) : one<CT>();
-      rp[t] = recip(pv[t]);
+    for (int i = 0; i < 4; ++i) xv[i] = rq0 + i < bs ? xs[rq0 + i] : zero<CT>();
+    // the lane's own 4 x 4 diagonal block (A[i][c] = Ud row rq0+i, col rq0+c),
+    // pivots 1 for rows past bs
+    CT dg[4][4], rpv[4], pvv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dg[i][c] = widen_to<CT>(Ud[(rq0 + i) + (rq0 + c) * LU]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      pvv[i] = rq0 + i < bs ? dg[i][i] : one<CT>();
+      rpv[i] = recip(pvv[i]);
     }
-    // Steps in groups of 8: the U entries of the next group (4 rows x 8
-    // pivots per lane) are loaded while the current group runs, so no shared
-    // memory load sits on the chain.  Rows and pivots past bs are inert
-    // (x = 0, U = 0, pivot 1), so the chain has no branch.
-    constexpr int GS = 8;
-    auto uload = [&](int g, CT (&u)[GS][4]) {
+    auto cload = [&](int g, CT (&u)[4][4]) {  // u[i][c] = Ud(rq0 + i, 4g + c)
 #pragma unroll
-      for (int e = 0; e < GS; ++e) {
-        const int jj = GS * g + e, jq = HERM ? jj : CZT - 1 - jj;
+      for (int c = 0; c < 4; ++c) {
+        const FT* cp = Ud + rq0 + (4 * g + c) * LU;
+        if constexpr (sizeof(FT) == 4) {
+          const float4 t4 = *reinterpret_cast<const float4*>(cp);
+          u[0][c] = widen_to<CT>(t4.x), u[1][c] = widen_to<CT>(t4.y);
+          u[2][c] = widen_to<CT>(t4.z), u[3][c] = widen_to<CT>(t4.w);
+        } else {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int rw = l + 32 * t;
-          u[e][t] = !HERM ? widen_to<CT>(Ud[rw + jq * LU]) : conj_(widen_to<CT>(Ud[jq + rw * LU]));
+          for (int i = 0; i < 4; ++i) u[i][c] = widen_to<CT>(cp[i]);
         }
       }
     };
-    CT ucur[GS][4];
-    uload(0, ucur);
+    constexpr int NG = CZT / 4;
+    // binary32 compute: the next group's entries are loaded one group ahead;
+    // wider types load them at the group start (registers), still ahead of
+    // the owner's 4 x 4 solve
+    constexpr bool AHEAD = sizeof(CT) == 4;
+    CT ucur[4][4];
+    if (AHEAD) cload(HERM ? 0 : NG - 1, ucur);
+#pragma unroll 4
+    for (int gg = 0; gg < NG; ++gg) {
+      const int g = HERM ? gg : NG - 1 - gg;
+      CT unext[AHEAD ? 4 : 1][AHEAD ? 4 : 1];
+      if (!AHEAD) cload(g, ucur);
+      if (AHEAD && gg + 1 < NG) cload(HERM ? g + 1 : g - 1, reinterpret_cast<CT(&)[4][4]>(unext));
+      if (l == g) {  // the 4 x 4 triangle: backward (U) or forward (U^H)
+        if (!HERM) {
 #pragma unroll
-    for (int g = 0; g < CZT / GS; ++g) {
-      CT unext[GS][4];
-      if (g + 1 < CZT / GS) uload(g + 1, unext);
+          for (int i = 3; i >= 0; --i) {
+            CT a = xv[i];
 #pragma unroll
-      for (int e = 0; e < GS; ++e) {
-        const int jj = GS * g + e, jq = HERM ? jj : CZT - 1 - jj;  // pivot row of this step
-        const int T = jq >> 5, jl = jq & 31;
-        const CT xj = shfl_idx(qdiv(xv[T], pv[T], rp[T]), jl);
-        if (l == jl) xv[T] = xj;
+            for (int c = 3; c > i; --c) a = a - dg[i][c] * xv[c];
+            xv[i] = qdiv(a, pvv[i], rpv[i]);
+          }
+        } else {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          // rows still to update: !HERM r < jq, HERM r > jq
-          const bool upd = !HERM ? (t < T || (t == T && l < jl)) : (t > T || (t == T && l > jl));
-          const CT d = xv[t] - ucur[e][t] * xj;
-          if (upd) xv[t] = d;
+          for (int i = 0; i < 4; ++i) {
+            CT a = xv[i];
+#pragma unroll
+            for (int c = 0; c < i; ++c) a = a - dg[i][c] * xv[c];
+            xv[i] = qdiv(a, pvv[i], rpv[i]);
+          }
         }
       }
-      if (g + 1 < CZT / GS)
+      CT xg[4];
 #pragma unroll
-        for (int e = 0; e < GS; ++e)
+      for (int c = 0; c < 4; ++c) xg[c] = shfl_idx(xv[c], g);
+      // rows still to update: !HERM lanes above the group, HERM lanes below
+      const bool upd = !HERM ? (l < g) : (l > g);
 #pragma unroll
-          for (int t = 0; t < 4; ++t) ucur[e][t] = unext[e][t];
+      for (int i = 0; i < 4; ++i) {
+        CT a = xv[i];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a = a - ucur[i][c] * xg[c];
+        if (upd) xv[i] = a;
+      }
+      if (AHEAD && gg + 1 < NG)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) ucur[i][c] = reinterpret_cast<CT(&)[4][4]>(unext)[i][c];
     }
     // publish x_j straight from the registers: the release by lane 0 after the
     // warp barrier covers the whole warp's stores
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (l + 32 * t < bs) x[i0 + l + 32 * t] = xv[t];
+    for (int i = 0; i < 4; ++i)
+      if (rq0 + i < bs) x[i0 + rq0 + i] = xv[i];
     __syncwarp();
     if (l == 0) st_release(flags + j, 1);
   }

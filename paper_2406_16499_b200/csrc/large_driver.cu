@@ -389,7 +389,7 @@ static bool trsv_persistent(const FT* M, int64_t ld, int64_t r0, int64_t c0, int
   if (!cascade_on() || !CzScratch::cnt || k <= 0) return false;
   const int K = (k + CZT - 1) / CZT;
   if (K > sm_count() || K > CZ_CNT) return false;
-  const size_t sm = sizeof(FT) * CZT * (CZT + 1) + sizeof(CT) * CZT * 6;
+  const size_t sm = sizeof(FT) * CZT * (CZT + 4) + sizeof(CT) * CZT * 6;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(k_trsv_chain<FT, CT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) ||

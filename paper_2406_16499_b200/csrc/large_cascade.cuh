@@ -541,5 +541,58 @@ __global__ void __launch_bounds__(CZ_NT, 1) k_trsv_chain(const FT* M, int64_t ld
   czstamp_any(4 * j + 2);
 }
 
+// ------------------------------------------------------------------ MGS
+// The modified Gram-Schmidt sweep of one GMRES step (gmres, krylov.hpp:436-512)
+// in one cooperative launch: for i = 0 .. k, h_i = <w, V_i>, w -= h_i V_i
+// (sequential in i, as MGS is), then h_{k+1} = <w, w>.  Thread e of the grid
+// owns entry e of w in a register; each dot is a warp butterfly, a fixed-
+// order sum over the CTA's warps, a per-step partial per CTA, one counter
+// barrier, and the partials summed in CTA order by every CTA (so all CTAs
+// subtract the same h_i).  V_{i+1}'s entry is loaded before the barrier.
+// part: 2 x gridDim.x doubles (double-buffered by step parity); cnt: one
+// int, zero at launch (arrival targets grow by gridDim.x per step).
+__global__ void __launch_bounds__(1024, 1) k_mgs(const double* Vb, int N, int k, double* w, double* h,
+                                                 double* part, int* cnt) {
+  __shared__ double red[32];
+  __shared__ double hsh;
+  const int tid = threadIdx.x, l = tid & 31, wi = tid >> 5;
+  const int c = blockIdx.x, G = gridDim.x;
+  const int e = c * 1024 + tid;
+  const bool in = e < N;
+  double we = in ? w[e] : 0.0;
+  double ve = (in && k >= 0) ? Vb[e] : 0.0;
+  for (int i = 0; i <= k + 1; ++i) {
+    const double y = i <= k ? ve : we;
+    double s = we * y;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (l == 0) red[wi] = s;
+    __syncthreads();
+    double* ps = part + (i & 1) * G;
+    if (tid == 0) {
+      double t = 0.0;
+#pragma unroll 8
+      for (int q = 0; q < 32; ++q) t += red[q];
+      ps[c] = t;
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(cnt) : "memory");
+    }
+    // the next basis vector's entry does not depend on this step
+    const double vn = (in && i + 1 <= k) ? Vb[int64_t(i + 1) * N + e] : 0.0;
+    if (tid == 0) {
+      while (ld_acquire(cnt) < (i + 1) * G) {
+      }
+      double hs = 0.0;
+      for (int q = 0; q < G; ++q) hs += ldcg_(ps + q);
+      hsh = hs;
+      if (c == 0) h[i] = hs;
+    }
+    __syncthreads();
+    const double hi = hsh;
+    if (i <= k) we = fma(-hi, ve, we);
+    ve = vn;
+  }
+  if (in) w[e] = we;
+}
+
 }  // namespace lg
 }  // namespace mlsb

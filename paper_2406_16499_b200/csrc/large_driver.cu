@@ -1094,6 +1094,21 @@ static void gm_cascade_gls(int n, int m, int p, const FT* M, int64_t ld, const F
   k_copy<double><<<nblk(m), KT, 0, st>>>(r1v, m, dx);
 }
 
+// One GMRES step's MGS sweep as a single cooperative launch (k_mgs); false
+// when it does not apply (MLSB_CASCADE_OLD, N beyond one 1024-row slice per
+// SM, no scratch) and the per-vector dot/axpy launches run instead.
+static bool mgs_fused(const double* Vb, int N, int k, double* w, double* h, double* part, int nb,
+                      cudaStream_t st) {
+  if (!cascade_on() || !CzScratch::cnt) return false;
+  const int G = (N + 1023) / 1024;
+  if (G > sm_count() || 2 * G > nb) return false;
+  int* cnt = CzScratch::cnt + 2 * (2 * CZ_CNT) + CZ_CNT - 1;  // lane 2's last trsv flag slot
+  if (cudaMemsetAsync(cnt, 0, sizeof(int), st) != cudaSuccess) return false;
+  void* args[] = {(void*)&Vb, (void*)&N, (void*)&k, (void*)&w, (void*)&h, (void*)&part, (void*)&cnt};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_mgs), dim3(G), dim3(1024), args, 0, st) ==
+         cudaSuccess;
+}
+
 // Full MGS-GMRES with Givens rotations (gmres, krylov.hpp:436-512; rel_tol
 // 1e-6, max_iter N) on the augmented system: `lp` is the left preconditioner
 // (or the split preconditioner's left half), `rp` the right half (kind 2);
@@ -1144,11 +1159,13 @@ static int gmres_core(int kind, int N, const double* rhs, double* wacc, const OP
         op(V(k), t4);
       }
       lp(t4, t2);
-      for (int i = 0; i <= k; ++i) {  // modified Gram-Schmidt
-        gm_dot(t2, V(i), N, part, nb, hdev + i, st);
-        k_axpy_dev<<<nblk(N), KT, 0, st>>>(hdev + i, V(i), N, t2);
+      if (!mgs_fused(bas.p, N, k, t2, hdev, part, nb, st)) {
+        for (int i = 0; i <= k; ++i) {  // modified Gram-Schmidt
+          gm_dot(t2, V(i), N, part, nb, hdev + i, st);
+          k_axpy_dev<<<nblk(N), KT, 0, st>>>(hdev + i, V(i), N, t2);
+        }
+        gm_dot(t2, t2, N, part, nb, hdev + k + 1, st);
       }
-      gm_dot(t2, t2, N, part, nb, hdev + k + 1, st);
       hh.assign(k + 2, 0.0);
       cudaMemcpyAsync(hh.data(), hdev, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, st);
       if ((e = cudaStreamSynchronize(st))) return MLSB_ERR_CUDA;

@@ -290,6 +290,12 @@ struct CzScratchGuard {
     CzScratch::lane = 0;
   }
 };
+// A second stream (and two events) for independent halves of the GMRES
+// preconditioners, set by solve() when the persistent kernels are in use.
+struct CzAux {
+  static inline thread_local cudaStream_t s = nullptr;
+  static inline thread_local cudaEvent_t fork = nullptr, join = nullptr;
+};
 struct CzLane {  // RAII: apply_F / trsv calls in this scope use lane `l`
   int prev;
   explicit CzLane(int l) : prev(CzScratch::lane) { CzScratch::lane = l; }
@@ -771,15 +777,34 @@ __global__ void k_finite_flag(const double* x, int n, int* flag) {
     if (!isfinite(x[i])) atomicOr(flag, 1);
 }
 
+// dst (rows x cols, ld rows) = src / s with exact division: the GMRES operator's
+// scaled copy of A, B (the reference scales a copy, krylov.hpp:557-563), made
+// once per solve so the operator streams it (k_resid_stream, multiply by 1.0)
+// instead of dividing every entry on every application
+__global__ void k_div_copy(const double* src, int64_t lds, int rows, int cols, double s, double* dst) {
+  const int64_t total = int64_t(rows) * cols;
+  for (int64_t e = int64_t(blockIdx.x) * KT + threadIdx.x; e < total; e += int64_t(gridDim.x) * KT) {
+    const int64_t j = e / rows, i = e - j * rows;
+    dst[e] = src[i + j * lds] / s;
+  }
+}
+
 // out = [alpha u1 + A u3; B u3; A^T u1 + B^T u2]  (augmented_operator::apply, krylov.hpp:62-77)
+// gA, gB: the exactly scaled copies (so sA = sB = 1 and the stream kernel's
+// scaling multiplies by 1.0); otherwise the raw inputs with exact division
 static void gm_op(int m, int n, int p, double alpha, const double* gA, const double* gB,
                   int64_t lda, int64_t ldb, double sA, double sB, const double* u, double* out,
                   double* rpart, double* cpart, cudaStream_t st) {
   const int R = m + p, C = n;
   const int ntr = (R + RTR - 1) / RTR, ntc = (C + RTC - 1) / RTC;
-  const StackX SX{gA, gB, lda, ldb, m, true, sA, sB};
   dim3 g2(ntr, ntc);
-  k_resid_tile<double, StackX><<<g2, KT, 0, st>>>(SX, R, C, u + R, u, rpart, cpart);
+  if (sA == 1.0 && sB == 1.0) {
+    const Stack<double> S{gA, gB, lda, ldb, m, true, 1.0, 1.0};
+    k_resid_stream<double><<<g2, KT, 0, st>>>(S, R, C, u + R, u, rpart, cpart);
+  } else {
+    const StackX SX{gA, gB, lda, ldb, m, true, sA, sB};
+    k_resid_tile<double, StackX><<<g2, KT, 0, st>>>(SX, R, C, u + R, u, rpart, cpart);
+  }
   k_op_reduce<<<nblk(R + C), KT, 0, st>>>(R, C, m, ntc, ntr, rpart, cpart, u, alpha, out);
 }
 
@@ -839,25 +864,42 @@ static void gm_bd(bool left, int m, int n, int p, double alpha, const FT* M, int
     k_scal<<<nblk(n), KT, 0, st>>>(sa, o3, n, o3);
     return;
   }
+  // the p-block (R solve) and the n-block (Q apply + T1 solve) are independent:
+  // the p-block runs on the auxiliary stream when there is one
+  cudaStream_t sp = CzAux::s ? CzAux::s : st;
+  if (CzAux::s) {
+    cudaEventRecord(CzAux::fork, st);
+    cudaStreamWaitEvent(sp, CzAux::fork, 0);
+  }
   if (left) {
-    k_copy<double><<<nblk(p), KT, 0, st>>>(w + m, p, ta);
-    trsv<FT, double>(M, ld, m, n - p, p, false, ta, st);                 // t = R^-1 w2
-    gemv_n<FT, double>(M, ld, n - p, p, n - p, p, up, ta, out + m, st);  // o2 = T(n-p:n, n-p:n) t
+    {
+      CzLane ln(CzAux::s ? 1 : CzScratch::lane);
+      k_copy<double><<<nblk(p), KT, 0, sp>>>(w + m, p, ta);
+      trsv<FT, double>(M, ld, m, n - p, p, false, ta, sp);                 // t = R^-1 w2
+      gemv_n<FT, double>(M, ld, n - p, p, n - p, p, up, ta, out + m, sp);  // o2 = T(n-p:n, n-p:n) t
+      k_scal<<<nblk(p), KT, 0, sp>>>(ra, out + m, p, out + m);
+    }
     k_copy<double><<<nblk(n), KT, 0, st>>>(w + m + p, n, tb);
     apply_F<FT, double>(FQ, true, tb, ypart, st);                        // q = Q w3
     trsv<FT, double>(M, ld, 0, 0, n, true, tb, st);                      // T1^T o3 = q
     k_scal<<<nblk(m), KT, 0, st>>>(ra, w, m, out);
-    k_scal<<<nblk(p), KT, 0, st>>>(ra, out + m, p, out + m);
     k_scal<<<nblk(n), KT, 0, st>>>(sa, tb, n, out + m + p);
   } else {
-    gemv_h<FT, double>(M, ld, n - p, p, n - p, p, up, w + m, ta, st);    // t = T(..)^T w2
-    trsv<FT, double>(M, ld, m, n - p, p, true, ta, st);                  // R^T o2 = t
+    {
+      CzLane ln(CzAux::s ? 1 : CzScratch::lane);
+      gemv_h<FT, double>(M, ld, n - p, p, n - p, p, up, w + m, ta, sp);    // t = T(..)^T w2
+      trsv<FT, double>(M, ld, m, n - p, p, true, ta, sp);                  // R^T o2 = t
+      k_scal<<<nblk(p), KT, 0, sp>>>(ra, ta, p, out + m);
+    }
     k_copy<double><<<nblk(n), KT, 0, st>>>(w + m + p, n, tb);
     trsv<FT, double>(M, ld, 0, 0, n, false, tb, st);                     // T1 t3 = w3
     apply_F<FT, double>(FQ, false, tb, ypart, st);                       // o3 = Q^T t3
     k_scal<<<nblk(m), KT, 0, st>>>(ra, w, m, out);
-    k_scal<<<nblk(p), KT, 0, st>>>(ra, ta, p, out + m);
     k_scal<<<nblk(n), KT, 0, st>>>(sa, tb, n, out + m + p);
+  }
+  if (CzAux::s) {
+    cudaEventRecord(CzAux::join, sp);
+    cudaStreamWaitEvent(st, CzAux::join, 0);
   }
 }
 
@@ -946,9 +988,14 @@ static void gm_op_gls(int n, int m, int p, double alpha, const double* gW, const
   const int ntr = (R + RTR - 1) / RTR, ntc = (C + RTC - 1) / RTC;
   k_copy<double><<<nblk(m), KT, 0, st>>>(u + p + n, m, tmp);
   k_copy<double><<<nblk(p), KT, 0, st>>>(u, p, tmp + m);
-  const StackX SX{gW, gV, ldw, ldv, m, false, sW, sV};
   dim3 g2(ntr, ntc);
-  k_resid_tile<double, StackX><<<g2, KT, 0, st>>>(SX, R, C, tmp, u + p, rpart, cpart);
+  if (sW == 1.0 && sV == 1.0) {
+    const Stack<double> S{gW, gV, ldw, ldv, m, false, 1.0, 1.0};
+    k_resid_stream<double><<<g2, KT, 0, st>>>(S, R, C, tmp, u + p, rpart, cpart);
+  } else {
+    const StackX SX{gW, gV, ldw, ldv, m, false, sW, sV};
+    k_resid_tile<double, StackX><<<g2, KT, 0, st>>>(SX, R, C, tmp, u + p, rpart, cpart);
+  }
   k_op_reduce_gls<<<nblk(p + n + m), KT, 0, st>>>(n, m, p, ntc, ntr, rpart, cpart, u, alpha, out);
 }
 
@@ -1567,6 +1614,17 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
     cudaStreamCreateWithFlags(&cs3, cudaStreamNonBlocking);
     for (int i = 0; i < 6; ++i) cudaEventCreateWithFlags(&cev[i], cudaEventDisableTiming);
   }
+  struct CzAuxGuard {
+    ~CzAuxGuard() {
+      CzAux::s = nullptr;
+      CzAux::fork = CzAux::join = nullptr;
+    }
+  } czaux_guard;
+  if (par && P.gmres) {  // GMRES preconditioners: their independent halves on cs2
+    CzAux::s = cs2;
+    CzAux::fork = cev[4];
+    CzAux::join = cev[5];
+  }
   // zero pivots in the order of the reference's first failing trsv
   // (LSE: R at lse.hpp:53, then T11 at :60; GLS: T22 at gls.hpp:55, then R at :61)
   const int kl = lse ? n - p : p - n + m;  // LSE: size of T11 ; GLS: column split of T
@@ -1680,7 +1738,10 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
   // x-block]; the Krylov basis grows on demand (full, unrestarted MGS-GMRES,
   // krylov.hpp:436-512, max_iter = N).
   const int N = m + p + n;
-  GmBuf gbuf, gbas;
+  GmBuf gbuf, gbas, gsc;
+  const double* gAs = nullptr;  // GMRES operator: exactly scaled copies
+  const double* gBs = nullptr;
+  int64_t ldas = 0, ldbs = 0;
   double *g_rhs = nullptr, *g_w = nullptr, *g_t1 = nullptr, *g_t2 = nullptr, *g_t3 = nullptr,
          *g_t4 = nullptr, *g_part = nullptr, *g_h = nullptr;
   int g_cap = 0;
@@ -1693,6 +1754,18 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       if ((e = cudaMallocAsync(reinterpret_cast<void**>(&gbuf.p),
                                sizeof(double) * (6 * nv + g_nb + 2 * (size_t(N) + 2)), st)))
         return MLSB_ERR_CUDA;
+      // exactly scaled copies of A, B (W, V) for the operator
+      const int sr1 = lse ? m : n, sc1 = lse ? n : m, sr2 = lse ? p : n, sc2 = lse ? n : p;
+      gsc.s = st;
+      if ((e = cudaMallocAsync(reinterpret_cast<void**>(&gsc.p),
+                               sizeof(double) * (size_t(sr1) * sc1 + size_t(sr2) * sc2), st)))
+        return MLSB_ERR_CUDA;
+      k_div_copy<<<148 * 8, KT, 0, st>>>(gA, P.lda, sr1, sc1, sA, gsc.p);
+      k_div_copy<<<148 * 8, KT, 0, st>>>(gB, P.ldb, sr2, sc2, sB, gsc.p + size_t(sr1) * sc1);
+      gAs = gsc.p;
+      gBs = gsc.p + size_t(sr1) * sc1;
+      ldas = sr1;
+      ldbs = sr2;
       g_rhs = gbuf.p;
       g_w = g_rhs + nv;
       g_t1 = g_w + nv;
@@ -1846,12 +1919,12 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
     if constexpr (kGm) {
       if (P.gmres) {
         int64_t its = 0;
-        int rc = lse ? gmres_correction(P.gmres, m, n, p, g_alpha, M, ld, FZ, FQ, gA, gB, P.lda, P.ldb, sA,
-                                        sB, rout, cout, sw, su, g_rhs, g_w, g_t1, g_t2, g_t3, g_t4, g_part,
+        int rc = lse ? gmres_correction(P.gmres, m, n, p, g_alpha, M, ld, FZ, FQ, gAs, gBs, ldas, ldbs, 1.0,
+                                        1.0, rout, cout, sw, su, g_rhs, g_w, g_t1, g_t2, g_t3, g_t4, g_part,
                                         g_nb, g_h, gbas, g_cap, cv, ypart, rpart, cpart, flags + 3, &its,
                                         st)
-                     : gmres_correction_gls(P.gmres, n, m, p, g_alpha, M, ld, FZ, FQ, gA, gB, P.lda, P.ldb,
-                                            sA, sB, rout, cout, sw, su, g_rhs, g_w, g_t1, g_t2, g_t3, g_t4,
+                     : gmres_correction_gls(P.gmres, n, m, p, g_alpha, M, ld, FZ, FQ, gAs, gBs, ldas, ldbs,
+                                            1.0, 1.0, rout, cout, sw, su, g_rhs, g_w, g_t1, g_t2, g_t3, g_t4,
                                             g_part, g_nb, g_h, gbas, g_cap, cv, ypart, rpart, cpart,
                                             flags + 3, &its, st);
         if (rc) return rc;

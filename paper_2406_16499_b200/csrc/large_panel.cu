@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelArgs<float> a) {
   __shared__ uint32_t rbase[PCL];                      // cluster address of xd in CTA c
   __shared__ __align__(16) float coef_s[NB];
   __shared__ float scal[2];
-  __shared__ float G[NB * NB];
+  __shared__ __align__(16) float G[NB * NB];
   __shared__ float taus[NB];
 
   cg::cluster_group cl = cg::this_cluster();
@@ -542,10 +542,18 @@ __global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelArgs<float> a) {
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
         if (q < nb) {
+          // column q of G as eight broadcast 16-byte loads, issued before the
+          // (unchanged, sequential) dot so no load latency sits on it
+          float gq[NB];
+#pragma unroll
+          for (int k4 = 0; k4 < NB; k4 += 4) {
+            const float4 g4 = *reinterpret_cast<const float4*>(&G[k4 + NB * q]);
+            gq[k4] = g4.x, gq[k4 + 1] = g4.y, gq[k4 + 2] = g4.z, gq[k4 + 3] = g4.w;
+          }
           float t = 0.f;
 #pragma unroll
           for (int k2 = 0; k2 < NB; ++k2)
-            if (k2 < q) t = fmaf(Tr[k2], G[k2 + NB * q], t);
+            if (k2 < q) t = fmaf(Tr[k2], gq[k2], t);
           const float tq = taus[q];
           Tr[q] = l < q ? -(tq * t) : (l == q ? tq : 0.f);
         }

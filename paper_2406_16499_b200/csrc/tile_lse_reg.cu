@@ -444,9 +444,13 @@ __device__ void build_T(float* G, const float* tau, int kb, int l) {
 #pragma unroll
   for (int q = 0; q < 32; ++q) {
     if (q < kb) {
+      // column q of G loaded before the (sequential) dot: no load latency on it
+      float gq[32];
+#pragma unroll
+      for (int k = 0; k < q; ++k) gq[k] = G[k + TLD * q];
       float t = 0.f;
 #pragma unroll
-      for (int k = 0; k < q; ++k) t = fmaf(Tr[k], G[k + TLD * q], t);
+      for (int k = 0; k < q; ++k) t = fmaf(Tr[k], gq[k], t);
       const float tq = tau[q];
       Tr[q] = (l < q) ? -tq * t : (l == q ? tq : 0.f);
     }

@@ -588,8 +588,12 @@ cudaError_t gemm_t(bool ha, bool hb, int M, int N, int K, T alpha, const T* A, i
 // (the block form of xLARFT's forward recursion).  G = V^H V comes from a
 // GEMM; one CTA merges the panels' T_jj (stored NB x NB, consecutive) in
 // shared memory.
+// one CTA of TMT threads: the merge is a chain of small triangular products
+// whose outputs are independent dot products, so more threads = more of them
+// in flight (round 1 ran 256 threads: ~53 us per outer block at C3)
+constexpr int TMT = 1024;
 template <class T>
-__global__ void __launch_bounds__(256) k_tmerge(int nbo, const T* __restrict__ G, int ldg,
+__global__ void __launch_bounds__(TMT) k_tmerge(int nbo, const T* __restrict__ G, int ldg,
                                                 const T* __restrict__ Tp, T* __restrict__ Tout,
                                                 int ldt) {
   extern __shared__ __align__(16) unsigned char sm_[];
@@ -599,16 +603,16 @@ __global__ void __launch_bounds__(256) k_tmerge(int nbo, const T* __restrict__ G
   const int tid = threadIdx.x;
   const int nblk = (nbo + NB - 1) / NB;
   // diagonal blocks: loads issued in batches of 16 from clamped addresses
-  for (int e0 = tid; e0 < nbo * nbo; e0 += 256 * 16) {
+  for (int e0 = tid; e0 < nbo * nbo; e0 += TMT * 16) {
     T v[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const int e = min(e0 + 256 * u, nbo * nbo - 1), r = e % nbo, c = e / nbo, br = r / NB;
+      const int e = min(e0 + TMT * u, nbo * nbo - 1), r = e % nbo, c = e / nbo, br = r / NB;
       v[u] = Tp[br * NB * NB + (r - br * NB) + (c % NB) * NB];
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const int e = e0 + 256 * u;
+      const int e = e0 + TMT * u;
       if (e < nbo * nbo) {
         const int r = e % nbo, c = e / nbo;
         S[r + c * LDS] = (r / NB == c / NB) ? v[u] : zero<T>();
@@ -619,28 +623,28 @@ __global__ void __launch_bounds__(256) k_tmerge(int nbo, const T* __restrict__ G
   T* GX = X + NBO * NB;  // staged block column G[0:h, c0:c0+w]
   for (int j = 1; j < nblk; ++j) {
     const int c0 = j * NB, w = min(NB, nbo - c0), h = c0;
-    for (int e0 = tid; e0 < h * w; e0 += 256 * 12) {
+    for (int e0 = tid; e0 < h * w; e0 += TMT * 12) {
       T v[12];
 #pragma unroll
       for (int u = 0; u < 12; ++u) {
-        const int e = min(e0 + 256 * u, h * w - 1);
+        const int e = min(e0 + TMT * u, h * w - 1);
         v[u] = G[e % h + int64_t(c0 + e / h) * ldg];
       }
 #pragma unroll
       for (int u = 0; u < 12; ++u) {
-        const int e = e0 + 256 * u;
+        const int e = e0 + TMT * u;
         if (e < h * w) GX[e % h + (e / h) * NBO] = v[u];
       }
     }
     __syncthreads();
-    for (int e = tid; e < h * w; e += 256) {
+    for (int e = tid; e < h * w; e += TMT) {
       const int r = e % h, c = e / h;
       T acc = zero<T>();
       for (int t = 0; t <= c; ++t) mac(acc, GX[r + t * NBO], S[(c0 + t) + (c0 + c) * LDS]);
       X[r + c * NBO] = acc;
     }
     __syncthreads();
-    for (int e = tid; e < h * w; e += 256) {
+    for (int e = tid; e < h * w; e += TMT) {
       const int r = e % h, c = e / h;
       T acc = zero<T>();
       for (int t = r; t < h; ++t) mac(acc, S[r + t * LDS], X[t + c * NBO]);
@@ -648,7 +652,7 @@ __global__ void __launch_bounds__(256) k_tmerge(int nbo, const T* __restrict__ G
     }
     __syncthreads();
   }
-  for (int e = tid; e < nbo * nbo; e += 256) {
+  for (int e = tid; e < nbo * nbo; e += TMT) {
     const int r = e % nbo, c = e / nbo;
     Tout[r + int64_t(c) * ldt] = S[r + c * LDS];
   }
@@ -665,7 +669,7 @@ static cudaError_t tmerge_t(int nbo, const T* G, int ldg, const T* Tp, T* Tout, 
     if (e) return e;
     attr = true;
   }
-  k_tmerge<T><<<1, 256, sm, st>>>(nbo, G, ldg, Tp, Tout, ldt);
+  k_tmerge<T><<<1, TMT, sm, st>>>(nbo, G, ldg, Tp, Tout, ldt);
   return cudaGetLastError();
 }
 cudaError_t tmerge_f32(int nbo, const float* G, int ldg, const float* Tp, float* Tout, int ldt,

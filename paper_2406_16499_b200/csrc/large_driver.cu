@@ -525,6 +525,140 @@ static int trail_cap() {
 }
 #define kTrailCap trail_cap()
 
+// Skinny compact-WY products of the inner updates (one panel's nbk <= 32
+// reflectors onto the <= 96 later columns / rows of its outer block).  As
+// three library-shaped GEMMs these cost a split-K GEMM + its reduction + a
+// one-tile T GEMM, each a mostly-idle launch on the look-ahead critical path;
+// here they are two kernels:
+//   k_skinny_part: P_g[k][n] = sum over CTA g's row chunks of op(V[r][k]) X(r, n)
+//     QR: X(r, n) = C2[r + n ld], op = conj  (P = V^H C2, nbk x nc)
+//     RQ: X(r, n) = Ma[n + r ld], op = id    (P = (Ma V)^T, nbk x nr)
+//   k_skinny_tmul: W = sum_g P_g in CTA order, then
+//     QR: W2 = T^H W (nbk x nc, ld nbk);  RQ: W2 = W^T T (nr x nbk, ld nr)
+// Neither needs co-residency: they run beside the capped trailing GEMM.
+constexpr int SK_RC = 64, SK_NT = 256, SK_NMAX = 96, SK_GMAX = 96, SK_VLD = 36;
+template <class FT, bool RQ>
+__global__ void __launch_bounds__(SK_NT) k_skinny_part(const FT* __restrict__ X, int64_t ld,
+                                                       const FT* __restrict__ V, int64_t ldv, int L, int nbk,
+                                                       int nc, FT* __restrict__ part) {
+  extern __shared__ __align__(16) unsigned char sk_sm[];
+  FT* Vs = reinterpret_cast<FT*>(sk_sm);  // [SK_RC][SK_VLD], V row-major
+  FT* Xs = Vs + SK_RC * SK_VLD;           // [nc][SK_RC + 1]
+  const int t = threadIdx.x, kq = t & 7, ng = t >> 3;
+  FT acc[3][4];
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[j][q] = zero<FT>();
+  const int nchunk = (L + SK_RC - 1) / SK_RC;
+  for (int ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
+    const int r0 = ch * SK_RC, rows = min(SK_RC, L - r0);
+    __syncthreads();
+    for (int i = t; i < SK_RC * 32; i += SK_NT) {
+      const int r = i % SK_RC, k = i / SK_RC;
+      Vs[r * SK_VLD + k] = (r < rows && k < nbk) ? V[r0 + r + k * ldv] : zero<FT>();
+    }
+    if (!RQ) {
+      for (int i = t; i < SK_RC * nc; i += SK_NT) {
+        const int r = i % SK_RC, n = i / SK_RC;
+        Xs[n * (SK_RC + 1) + r] = r < rows ? X[r0 + r + n * ld] : zero<FT>();
+      }
+    } else {
+      for (int i = t; i < SK_RC * nc; i += SK_NT) {
+        const int n = i % nc, r = i / nc;
+        Xs[n * (SK_RC + 1) + r] = r < rows ? X[n + (r0 + r) * ld] : zero<FT>();
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int r = 0; r < SK_RC; ++r) {
+      FT v[4];
+      if constexpr (sizeof(FT) == 4) {
+        const float4 q4 = *reinterpret_cast<const float4*>(Vs + r * SK_VLD + 4 * kq);
+        v[0] = q4.x, v[1] = q4.y, v[2] = q4.z, v[3] = q4.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = Vs[r * SK_VLD + 4 * kq + q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!RQ) v[q] = conj_(v[q]);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int n = ng + 32 * j;
+        if (n < nc) {
+          const FT x = Xs[n * (SK_RC + 1) + r];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) mac(acc[j][q], v[q], x);
+        }
+      }
+    }
+  }
+  FT* P = part + size_t(blockIdx.x) * 32 * nc;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const int n = ng + 32 * j;
+    if (n < nc)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) P[4 * kq + q + 32 * n] = acc[j][q];
+  }
+}
+
+template <class FT, bool RQ>
+__global__ void __launch_bounds__(128) k_skinny_tmul(const FT* __restrict__ part, int G, int nbk, int nc,
+                                                     const FT* __restrict__ T, int ldt, FT* __restrict__ W2) {
+  __shared__ FT ws[4][32];
+  const int w = threadIdx.x >> 5, k = threadIdx.x & 31, n = blockIdx.x * 4 + w;
+  if (n >= nc) return;  // whole warp
+  const FT* p = part + k + 32 * n;
+  const size_t gs = size_t(32) * nc;
+  FT s = zero<FT>();
+  int g = 0;
+  for (; g + 8 <= G; g += 8) {
+    FT b[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) b[i] = p[(g + i) * gs];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s = s + b[i];
+  }
+  for (; g < G; ++g) s = s + p[g * gs];
+  ws[w][k] = s;
+  __syncwarp();
+  if (k >= nbk) return;
+  FT o = zero<FT>();
+  for (int kk = 0; kk <= k; ++kk) {
+    const FT tv = T[kk + int64_t(ldt) * k];
+    mac(o, RQ ? tv : conj_(tv), ws[w][kk]);
+  }
+  if (!RQ) W2[k + int64_t(nbk) * n] = o;
+  else W2[n + int64_t(nc) * k] = o;
+}
+
+static bool skinny_on() {
+  static const bool v = getenv("MLSB_SKINNY_OLD") == nullptr;
+  return v;
+}
+template <class FT>
+static bool skinny_fits(int L, int nbk, int nc, const WsBuf& w) {
+  const int G = std::min((L + SK_RC - 1) / SK_RC, SK_GMAX);
+  return skinny_on() && nbk <= 32 && nc > 0 && nc <= SK_NMAX && L > 0 && size_t(G) * 32 * nc <= w.wn;
+}
+// W2 of an inner update (skinny_fits must hold)
+template <class FT, bool RQ>
+static cudaError_t skinny_w2(const FT* X, int64_t ld, const FT* V, int64_t ldv, int L, int nbk, int nc,
+                             const FT* Tb, int ldt, FT* W2, const WsBuf& w, cudaStream_t st) {
+  constexpr size_t smax = (SK_RC * SK_VLD + SK_NMAX * (SK_RC + 1)) * sizeof(FT);
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_skinny_part<FT, RQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smax));
+  if (attr) return attr;
+  const int G = std::min((L + SK_RC - 1) / SK_RC, SK_GMAX);
+  const size_t sm = (SK_RC * SK_VLD + size_t(nc) * (SK_RC + 1)) * sizeof(FT);
+  FT* part = static_cast<FT*>(w.work);
+  k_skinny_part<FT, RQ><<<G, SK_NT, sm, st>>>(X, ld, V, ldv, L, nbk, nc, part);
+  k_skinny_tmul<FT, RQ><<<(nc + 3) / 4, 128, 0, st>>>(part, G, nbk, nc, Tb, ldt, W2);
+  return cudaGetLastError();
+}
+
 // C2 := P^H C2 = C2 - V T^H (V^H C2) for C2 = M[j0:j0+L, c0:c0+nc]
 template <class FT>
 static cudaError_t qr_update(FT* M, int64_t ld, int j0, int L, int nbk, int c0, int nc, const FT* V,
@@ -535,6 +669,10 @@ static cudaError_t qr_update(FT* M, int64_t ld, int j0, int L, int nbk, int c0, 
   FT* W2 = static_cast<FT*>(w.W2);
   FT* work = static_cast<FT*>(w.work);
   FT* C2 = M + j0 + int64_t(c0) * ld;
+  if (skinny_fits<FT>(L, nbk, nc, w)) {
+    if ((e = skinny_w2<FT, false>(C2, ld, V, ldv, L, nbk, nc, Tb, ldt, W2, w, st))) return e;
+    return gemm<FT>(false, false, L, nc, nbk, -1.0, V, ldv, W2, nbk, 1.0, C2, ld, nullptr, 0, st);
+  }
   if ((e = gemm<FT>(true, false, nbk, nc, L, 1.0, V, ldv, C2, ld, 0.0, W, nbk, work, w.wn, st))) return e;
   if ((e = gemm<FT>(true, false, nbk, nc, nbk, 1.0, Tb, ldt, W, nbk, 0.0, W2, nbk, nullptr, 0, st))) return e;
   return gemm<FT>(false, false, L, nc, nbk, -1.0, V, ldv, W2, nbk, 1.0, C2, ld, nullptr, 0, st);
@@ -550,6 +688,10 @@ static cudaError_t rq_update(FT* M, int64_t ld, int r0, int nr, int cb, int L, i
   FT* W2 = static_cast<FT*>(w.W2);
   FT* work = static_cast<FT*>(w.work);
   FT* Ma = M + r0 + int64_t(cb) * ld;
+  if (skinny_fits<FT>(L, nbk, nr, w)) {
+    if ((e = skinny_w2<FT, true>(Ma, ld, V, ldv, L, nbk, nr, Tb, ldt, W2, w, st))) return e;
+    return gemm<FT>(false, true, nr, L, nbk, -1.0, W2, nr, V, ldv, 1.0, Ma, ld, nullptr, 0, st);
+  }
   if ((e = gemm<FT>(false, false, nr, nbk, L, 1.0, Ma, ld, V, ldv, 0.0, W, nr, work, w.wn, st))) return e;
   if ((e = gemm<FT>(false, false, nr, nbk, nbk, 1.0, W, nr, Tb, ldt, 0.0, W2, nr, nullptr, 0, st))) return e;
   return gemm<FT>(false, true, nr, L, nbk, -1.0, W2, nr, V, ldv, 1.0, Ma, ld, nullptr, 0, st);

@@ -46,6 +46,9 @@ def test_dropin_demo_exception_path_without_gpu():
 
 HARN_GPU = os.path.join(ROOT, "oracle", "_ref", "b200_harness")
 HARN_REF = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
+# m + n + p + 1 of the desk-scale sweep shapes (inc/experiment.hpp:220-260):
+# LSE (2048, 256, 8), GLS (1024, 32, 1152)
+DESK_N = {"lse": 2048 + 256 + 8 + 1, "gls": 1024 + 32 + 1152 + 1}
 CELL = re.compile(r"CELL (\d+) kind (\w+) cond (\S+) method (\S+) status (\w+) iters (\d+) inner (\d+) m1 (\S+) m2 (\S+)")
 
 
@@ -88,7 +91,16 @@ def test_reference_run_sweep_routed_to_b200(gpu, kind):
             bad.append((a, b))
             continue
         if st_g == "converged":
-            for k in (7, 8):
-                if not float(a[k]) <= max(10 * float(b[k]), 1e-12):
-                    bad.append(("metric", k, a, b))
+            # m1 (err-1 / er-1, a backward-type error): within 10x of the
+            # reference.  m2 (err-2 / er-2) is the forward error against the
+            # binary64 direct solution: the parity bar of north_star,
+            # c * N * u_r * kappa (tests/helpers.py), or within 10x -- a run that
+            # stops one pass earlier (both below tol) legitimately ends with a
+            # forward error many times the other run's at kappa >= 1e5
+            cond = float(a[2])
+            fwd_bound = 40 * DESK_N[kind] * 2.0 ** -53 * cond
+            if not float(a[7]) <= max(10 * float(b[7]), 1e-12):
+                bad.append(("metric", 7, a, b))
+            if not float(a[8]) <= max(10 * float(b[8]), fwd_bound, 1e-12):
+                bad.append(("metric", 8, a, b))
     assert not bad, bad

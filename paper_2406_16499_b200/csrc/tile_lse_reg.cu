@@ -34,6 +34,11 @@ namespace reg {
 constexpr int NT = 512, NW = 16;
 constexpr int RT = 9, CS = 8;         // register tile: rows l+32t (t<RT), cols w+16s (s<CS)
 constexpr int RMAX = 32 * RT;         // 288
+// The QR register tile is held as column pairs (slots s, s+1 of a row slot in
+// one aligned register pair) so the bulk dot products and rank-1 updates are
+// packed FFMA2 (fma.rn.f32x2): two independent binary32 FMAs per instruction,
+// each with the operands and rounding of the scalar fmaf it replaces.
+#define AR(t, s) ((((s) & 1) != 0) ? ar[t][(s) >> 1].y : ar[t][(s) >> 1].x)
 constexpr int CMAX = NW * CS;         // 128
 constexpr int NWORK = 7;              // solve-precision work vectors
 constexpr int RH = 160;               // residual: rows per row-half
@@ -559,18 +564,20 @@ __device__ __forceinline__ Col9 gen_col_core(Col9 col, int jc, int m, int l, flo
   return col;
 }
 template <int SC>
-__device__ __forceinline__ void gen_col(float (&ar)[RT][CS], int jc, int m, int l, float* vout,
+__device__ __forceinline__ void gen_col(float2 (&ar)[RT][CS / 2], int jc, int m, int l, float* vout,
                                         float* tau1) {
   Col9 c;
 #pragma unroll
-  for (int t = 0; t < RT; ++t) c.v[t] = ar[t][SC];
+  for (int t = 0; t < RT; ++t) c.v[t] = AR(t, SC);
   c = gen_col_core<SC / 2>(c, jc, m, l, vout, tau1);
 #pragma unroll
-  for (int t = 0; t < RT; ++t) ar[t][SC] = c.v[t];
+  for (int t = 0; t < RT; ++t) AR(t, SC) = c.v[t];
 }
 
 // RQ layout: lane l <-> columns l + 32 s (s < BS), warp w <-> rows w + 16 t (t < BT)
 constexpr int BT = 18, BS = 4;
+// RQ register tile as row pairs (row slots t, t+1), packed like the QR tile
+#define BR(t, s) ((((t) & 1) != 0) ? br[(t) >> 1][s].y : br[(t) >> 1][s].x)
 static_assert(BS == 4, "rq_crit's dot is written for 4 column slots");
 
 // RQ reflector of row m+j held by its owner warp (lane l holds columns
@@ -610,14 +617,14 @@ __device__ __forceinline__ Row4 gen_row_core(Row4 row, int j, int pc, int C, int
   return row;
 }
 template <int TO>
-__device__ __forceinline__ void gen_row(float (&br)[BT][BS], int j, int pc, int C, int l,
+__device__ __forceinline__ void gen_row(float2 (&br)[BT / 2][BS], int j, int pc, int C, int l,
                                         float* vout, float* tau2) {
   Row4 r;
 #pragma unroll
-  for (int s = 0; s < BS; ++s) r.v[s] = br[TO][s];
+  for (int s = 0; s < BS; ++s) r.v[s] = BR(TO, s);
   r = gen_row_core(r, j, pc, C, l, vout, tau2);
 #pragma unroll
-  for (int s = 0; s < BS; ++s) br[TO][s] = r.v[s];
+  for (int s = 0; s < BS; ++s) BR(TO, s) = r.v[s];
 }
 
 // 16 partial sums per lane -> every lane gets all 16 sums
@@ -676,16 +683,16 @@ constexpr int NVB = 4;
 // RQ owner path: apply reflector (vv, tj) to the owner's row slot TO, then
 // generate the next reflector (index jn, pivot pc, sequence number kn) from it.
 template <int TO>
-__device__ __forceinline__ void rq_crit(float (&br)[BT][BS], const float (&vv)[BS], float tj, int jn,
+__device__ __forceinline__ void rq_crit(float2 (&br)[BT / 2][BS], const float (&vv)[BS], float tj, int jn,
                                         int pc, int C, int l, float* vbuf, float* tau2,
                                         uint64_t* full, uint64_t* empty, int kn) {
   const int b = kn % NVB;
   if (kn >= NVB) mbar_wait(empty + b, ((kn / NVB) - 1) & 1);  // (long satisfied: off the chain)
-  const float dc = warp_sum(fmaf(br[TO][0], vv[0], br[TO][1] * vv[1]) +
-                           fmaf(br[TO][2], vv[2], br[TO][3] * vv[3]));
+  const float dc = warp_sum(fmaf(BR(TO, 0), vv[0], BR(TO, 1) * vv[1]) +
+                           fmaf(BR(TO, 2), vv[2], BR(TO, 3) * vv[3]));
   if (tj != 0.f)
 #pragma unroll
-    for (int s = 0; s < BS; ++s) br[TO][s] = fmaf(-(tj * vv[s]), dc, br[TO][s]);
+    for (int s = 0; s < BS; ++s) BR(TO, s) = fmaf(-(tj * vv[s]), dc, BR(TO, s));
   gen_row<TO>(br, jn, pc, C, l, vbuf + b * CMAX, tau2);
   __syncwarp();  // orders the warp's stores of v and tau before lane 0's release
   if (l == 0) mbar_arrive(full + b);
@@ -698,7 +705,7 @@ __device__ __forceinline__ void rq_crit(float (&br)[BT][BS], const float (&vv)[B
 // reduction (v_j vanishes past its pivot, where v_k still holds explicit
 // entries).
 template <int TO>
-__device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p, int C, int w,
+__device__ __forceinline__ void rq_slot(float2 (&br)[BT / 2][BS], int m, int n, int p, int C, int w,
                                         int l, float* vbuf, float* tau2, float* TQ, uint64_t* full,
                                         uint64_t* empty) {
   if (NW * TO + NW - 1 < m || NW * TO >= m + p) return;  // no reflector rows in this slot
@@ -729,18 +736,18 @@ __device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p
         rq_crit<(TO > 0 ? TO - 1 : 0)>(br, vv, tj, j - 1, n - p + j - 1, C, l, vbuf, tau2, full,
                                        empty, k + 1);
     }
-    float d[16], e0 = 0.f, e1 = 0.f;
+    // row-pair dots: dd[q] = (row 2q, row 2q+1) . v, one FFMA2 per column slot
+    float2 dd[BT / 2];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      d[t] = 0.f;
+    for (int q = 0; q < BT / 2; ++q) {
+      dd[q] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int s = 0; s < BS; ++s) d[t] = fmaf(br[t][s], vv[s], d[t]);
+      for (int s = 0; s < BS; ++s) dd[q] = __ffma2_rn(br[q][s], make_float2(vv[s], vv[s]), dd[q]);
     }
+    float d[16];
 #pragma unroll
-    for (int s = 0; s < BS; ++s) {
-      e0 = fmaf(br[16][s], vv[s], e0);
-      e1 = fmaf(br[17][s], vv[s], e1);
-    }
+    for (int t = 0; t < 16; ++t) d[t] = (t & 1) ? dd[t >> 1].y : dd[t >> 1].x;
+    float e0 = dd[8].x, e1 = dd[8].y;
     __syncwarp();
     if (l == 0) mbar_arrive(empty + b);
     reduce16(d, l);
@@ -749,9 +756,23 @@ __device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p
     const int jb = j & ~31;
     // rows above the reflector row are updated (the owner's row - 1 already
     // was); rows below it only give Gram entries.  tj == 0 means v = e_pc, whose
-    // update adds exact zeros, so the update is branch-free.
+    // update adds exact zeros, so the update is branch-free.  Row pairs wholly
+    // above every reflector row of this slot (2q + 2 < TO) take one FFMA2 per
+    // column slot; the pairs at the slot boundary go row by row.
+#pragma unroll
+    for (int q = 0; q < BT / 2; ++q) {
+      if (2 * q + 2 < TO) {
+        const float2 dq = make_float2(q < 8 ? d[2 * q] : e0, q < 8 ? d[2 * q + 1] : e1);
+#pragma unroll
+        for (int s = 0; s < BS; ++s) {
+          const float ms = -(tj * vv[s]);
+          br[q][s] = __ffma2_rn(dq, make_float2(ms, ms), br[q][s]);
+        }
+      }
+    }
 #pragma unroll
     for (int t = 0; t < BT; ++t) {
+      if ((t | 1) + 1 < TO) continue;  // done by the pair loop
       const int i = w + NW * t;
       const float dt = t < 16 ? d[t < 16 ? t : 0] : (t == 16 ? e0 : e1);
       const bool above = t < TO || (t == TO && w < wo);
@@ -759,7 +780,7 @@ __device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p
       const bool skip = own && (t == TO ? wo > 0 : (t == TO - 1 && wo == 0));
       if (above && !skip) {
 #pragma unroll
-        for (int s = 0; s < BS; ++s) br[t][s] = fmaf(-(tj * vv[s]), dt, br[t][s]);
+        for (int s = 0; s < BS; ++s) BR(t, s) = fmaf(-(tj * vv[s]), dt, BR(t, s));
       } else if (below && i < m + p) {
         const int kk = i - m;
         if (l == 0 && (kk & ~31) == jb) TQ[(jb >> 5) * TSZ + (j - jb) + TLD * (kk - jb)] = dt;
@@ -771,7 +792,7 @@ __device__ __forceinline__ void rq_slot(float (&br)[BT][BS], int m, int n, int p
 // QR owner path: apply reflector j (vr, tj) to column j1 = j + 1 in slot S1,
 // then generate reflector j1 from it.
 template <int S1, int T0>
-__device__ __forceinline__ void qr_crit(float (&ar)[RT][CS], const float (&vr)[RT], float tj, int j1,
+__device__ __forceinline__ void qr_crit(float2 (&ar)[RT][CS / 2], const float (&vr)[RT], float tj, int j1,
                                         int m, int l, float* vbuf, float* tau1, uint64_t* full,
                                         uint64_t* empty) {
   const int b = j1 % NVB;
@@ -779,7 +800,7 @@ __device__ __forceinline__ void qr_crit(float (&ar)[RT][CS], const float (&vr)[R
   float dc = 0.f;
 #pragma unroll
   for (int t = T0; t < RT; ++t)
-    if (32 * t < m) dc = fmaf(ar[t][S1], vr[t], dc);
+    if (32 * t < m) dc = fmaf(AR(t, S1), vr[t], dc);
   dc = warp_sum(dc);
   // probe layout (steps j1 = 33..64): [j1-33] warp_sum done, [32+..] update done,
   // [64+..] gen done, [96+..] published
@@ -793,7 +814,7 @@ __device__ __forceinline__ void qr_crit(float (&ar)[RT][CS], const float (&vr)[R
     const float sc = tj * dc;
 #pragma unroll
     for (int t = T0; t < RT; ++t)
-      if (32 * t < m) ar[t][S1] = fmaf(-sc, vr[t], ar[t][S1]);
+      if (32 * t < m) AR(t, S1) = fmaf(-sc, vr[t], AR(t, S1));
   }
   if (pb >= 0) PROBE(pb + 32);
   gen_col<S1>(ar, j1, m, l, vbuf + b * RMAX, tau1);
@@ -808,7 +829,7 @@ __device__ __forceinline__ void qr_crit(float (&ar)[RT][CS], const float (&vr)[R
 // rows >= j live in row slots t >= SC/2, and columns >= the Gram block start
 // live in slots s >= SC & ~1, so finished rows/columns cost no instructions.
 template <int SC>
-__device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int kz, int w, int l,
+__device__ __forceinline__ void qr_slot(float2 (&ar)[RT][CS / 2], int m, int C, int kz, int w, int l,
                                         float* vbuf, float* tau1, float* TZ, uint64_t* full,
                                         uint64_t* empty) {
   constexpr int T0 = SC / 2, S0 = SC & ~1;
@@ -835,15 +856,19 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
       else qr_crit<(SC + 1 < CS ? SC + 1 : SC), T0>(ar, vr, tj, j1, m, l, vbuf, tau1, full, empty);
     }
     constexpr int bstart = NW * S0;  // j & ~31
-    float d[CS];
+    // column-pair dots (S0 is even): one FFMA2 per row slot and pair
+    float2 dp[CS / 2];
 #pragma unroll
-    for (int s = 0; s < CS; ++s) d[s] = 0.f;
+    for (int q = 0; q < CS / 2; ++q) dp[q] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int t = T0; t < RT; ++t) {
       if (32 * t >= m) continue;
 #pragma unroll
-      for (int s = S0; s < CS; ++s) d[s] = fmaf(ar[t][s], vr[t], d[s]);
+      for (int q = S0 / 2; q < CS / 2; ++q) dp[q] = __ffma2_rn(ar[t][q], make_float2(vr[t], vr[t]), dp[q]);
     }
+    float d[CS];
+#pragma unroll
+    for (int s = 0; s < CS; ++s) d[s] = (s & 1) ? dp[s >> 1].y : dp[s >> 1].x;
     __syncwarp();
     if (l == 0) mbar_arrive(empty + b);
     constexpr int NL = CS - S0 > 4 ? 8 : (CS - S0 > 2 ? 4 : 2);
@@ -854,8 +879,24 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
     // column j1 (slot SC, or SC + 1 when jw is the last warp).  tj == 0 means
     // v = e_j, whose update adds exact zeros, so the update is branch-free.
     const bool own_sc = own && jw < NW - 1, own_sc1 = own && jw == NW - 1;
+    // column pairs past slot SC + 1 hold live columns only: one FFMA2 per row
+    // slot (when both columns exist); the pairs at SC, SC + 1 go column by column
+    constexpr int QF = (SC + 2 + 1) / 2;  // first pair with 2q > SC + 1
+    bool pair_done[CS / 2];
+#pragma unroll
+    for (int q = 0; q < CS / 2; ++q) {
+      pair_done[q] = false;
+      if (q >= QF && q >= S0 / 2 && NW * (2 * q + 2) <= C) {
+        const float m0 = -(tj * d[2 * q]), m1 = -(tj * d[2 * q + 1]);
+#pragma unroll
+        for (int t = T0; t < RT; ++t)
+          if (32 * t < m) ar[t][q] = __ffma2_rn(make_float2(m0, m1), make_float2(vr[t], vr[t]), ar[t][q]);
+        pair_done[q] = true;
+      }
+    }
 #pragma unroll
     for (int s = S0; s < CS; ++s) {
+      if (pair_done[s >> 1]) continue;
       const int c = w + NW * s;
       const bool gram = s < SC || (s == SC && w < jw);
       const bool live = s > SC + 1 || (s == SC && w > jw && !own_sc) || (s == SC + 1 && !own_sc1);
@@ -866,7 +907,7 @@ __device__ __forceinline__ void qr_slot(float (&ar)[RT][CS], int m, int C, int k
         const float sc = tj * d[s];
 #pragma unroll
         for (int t = T0; t < RT; ++t)
-          if (32 * t < m) ar[t][s] = fmaf(-sc, vr[t], ar[t][s]);
+          if (32 * t < m) AR(t, s) = fmaf(-sc, vr[t], AR(t, s));
       }
     }
   }
@@ -1044,13 +1085,13 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     // ------------------------------------------ RQ of the B rows (bottom-up), layout B
     // (rq(B) and C = A Q^T of factor.hpp:34-52 in one sweep over every row above)
     {
-      float br[BT][BS];
+      float2 br[BT / 2][BS];
 #pragma unroll
       for (int t = 0; t < BT; ++t)
 #pragma unroll
         for (int s = 0; s < BS; ++s) {
           const int i = w + NW * t, c = l + 32 * s;
-          br[t][s] = (i < R && c < C) ? M[i + size_t(c) * ld] : 0.f;
+          BR(t, s) = (i < R && c < C) ? M[i + size_t(c) * ld] : 0.f;
         }
       rq_slot<17>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
       rq_slot<16>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
@@ -1076,7 +1117,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
 #pragma unroll
         for (int s = 0; s < BS; ++s) {
           const int i = w + NW * t, c = l + 32 * s;
-          if (i < R && c < C) M[i + size_t(c) * ld] = br[t][s];
+          if (i < R && c < C) M[i + size_t(c) * ld] = BR(t, s);
         }
     }
     __syncthreads();
@@ -1087,13 +1128,13 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
 
     // ------------------------------------------ QR of C = M[0:m, 0:n], layout A
     {
-      float ar[RT][CS];
+      float2 ar[RT][CS / 2];
 #pragma unroll
       for (int s = 0; s < CS; ++s)
 #pragma unroll
         for (int t = 0; t < RT; ++t) {
           const int i = l + 32 * t, c = w + NW * s;
-          ar[t][s] = (i < R && c < C) ? M[i + size_t(c) * ld] : 0.f;
+          AR(t, s) = (i < R && c < C) ? M[i + size_t(c) * ld] : 0.f;
         }
       qr_slot<0>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
       qr_slot<1>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
@@ -1110,7 +1151,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
 #pragma unroll
         for (int t = 0; t < RT; ++t) {
           const int i = l + 32 * t, c = w + NW * s;
-          if (i < R && c < C) M[i + size_t(c) * ld] = ar[t][s];
+          if (i < R && c < C) M[i + size_t(c) * ld] = AR(t, s);
         }
     }
   }

@@ -227,16 +227,25 @@ struct Arena {
   char* base = nullptr;
   size_t used = 0, cap = 0;
   cudaStream_t st = nullptr;
+  // debug (MLSB_POISON=1): the arena starts as huge finite garbage instead of
+  // whatever the pool held, so a read of a never-written entry shows up;
+  // MLSB_POISON_ZERO=i zeroes the i-th take() again (bisection)
+  int ntake = 0;
   cudaError_t init(size_t bytes, cudaStream_t s) {
     st = s;
     cap = bytes;
-    return cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, s);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, s);
+    if (!e && getenv("MLSB_POISON")) e = cudaMemsetAsync(base, 0x7F, bytes, s);
+    return e;
   }
   template <class T> T* take(size_t n) {
     used = (used + 255) & ~size_t(255);
     T* p = reinterpret_cast<T*>(base + used);
     used += n * sizeof(T);
-    return used <= cap ? p : nullptr;
+    if (used > cap) return nullptr;
+    static const int zi = getenv("MLSB_POISON_ZERO") ? atoi(getenv("MLSB_POISON_ZERO")) : -1;
+    if (ntake++ == zi && getenv("MLSB_POISON")) cudaMemsetAsync(p, 0, n * sizeof(T), st);
+    return p;
   }
   ~Arena() {
     if (base) cudaFreeAsync(base, st);
@@ -2226,9 +2235,11 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
         trsv<FT, CT>(M, ld, 0, 0, m, false, r1v, cs3);                  // R dx = ...
       }
       trsv<FT, CT>(M, ld, m, m + kp, nm, true, r2, st);                 // T22^H h2 = ...
-      k_copy<CT><<<nblk(m), KT, 0, st>>>(h1, m, u);
-      k_copy<CT><<<nblk(nm), KT, 0, st>>>(r2, nm, u + m);
-      apply_F<FT, CT>(FZ, false, u, ypart, st);                          // Q [h1; h2]
+      // [h1; h2] is assembled in w (free since the elementwise step above), not
+      // in u as the serial order does: the third stream's k_sub2 still reads u
+      k_copy<CT><<<nblk(m), KT, 0, st>>>(h1, m, w);
+      k_copy<CT><<<nblk(nm), KT, 0, st>>>(r2, nm, w + m);
+      apply_F<FT, CT>(FZ, false, w, ypart, st);                          // Q [h1; h2]
       cudaEventRecord(cev[4], cs2);
       cudaEventRecord(cev[5], cs3);
       cudaStreamWaitEvent(st, cev[4], 0);
@@ -2236,7 +2247,7 @@ static int solve(const LargeProblem& P, cudaStream_t st, LargeOut* out) {
       mark("phaseB");
       k_promote_add<WT, CT><<<nblk(m), KT, 0, st>>>(su, m, r1v, sb, false, flags + 3);
       k_promote_add<WT, CT><<<nblk(p), KT, 0, st>>>(su + m, p, hh, sb, false, flags + 3);
-      k_promote_add<WT, CT><<<nblk(n), KT, 0, st>>>(sw, n, u, sb, true, flags + 3);  // dz = -Q h
+      k_promote_add<WT, CT><<<nblk(n), KT, 0, st>>>(sw, n, w, sb, true, flags + 3);  // dz = -Q h
     } else {    // Algorithm 3 (gls.hpp:106-154)
       const int nm = n - m, kp = kl;
       const int kk = std::min(n, p);

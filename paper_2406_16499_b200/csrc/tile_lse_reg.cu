@@ -78,7 +78,7 @@ __host__ __device__ inline Layout make_layout(int64_t m, int64_t n, int64_t p, i
   L.oCout = o;  o = al16(o + size_t(CMAX) * 8);
   L.oSu = o;    o = al16(o + size_t(CMAX) * 8);
   L.oWork = o;  o = al16(o + size_t(NWORK) * RMAX * csz);
-  L.oRed = o;   o = al16(o + size_t(NW) * 8 * 8);
+  L.oRed = o;   o = al16(o + size_t(NW) * 9 * 8);  // [NW][8] sums + [NW] maxima
   L.oScal = o;  o = al16(o + 64 * 8);
   L.oRinv = o;  o = al16(o + size_t(2) * CMAX * csz + size_t(2) * CMAX * 4);
   L.total = o;
@@ -94,7 +94,7 @@ enum Slot { S_SA = 0, S_SB, S_CB, S_CD, S_NB, S_ND, S_NA, S_NBF, S_SIG, S_BETA, 
 // per-lane partial sums: k pair-halving exchanges, 5 - k plain exchanges,
 // then N broadcasts; every lane returns all N sums (fixed order).
 template <int S0, int N>
-__device__ __forceinline__ void reduce_live(float (&d)[8], int l) {
+__device__ __forceinline__ void reduce_live(float (&d)[8], int l, float* sc) {
   static_assert(N == 8 || N == 4 || N == 2, "N");
   float e[N];
 #pragma unroll
@@ -117,9 +117,76 @@ __device__ __forceinline__ void reduce_live(float (&d)[8], int l) {
 #pragma unroll
   for (int o = 16 >> K; o >= 1; o >>= 1) e[0] += __shfl_xor_sync(0xffffffffu, e[0], o);
   const float mine = e[0];
+  if (N >= 4) {
+    // the N sums go back to every lane through the warp's scratch (one store,
+    // N / 4 broadcast 16-byte loads) instead of N shuffles; `sc` alternates
+    // between two buffers from step to step, so the __syncwarp below also
+    // separates this store from the loads of two steps ago
+    if ((l & ((32 >> K) - 1)) == 0) sc[l >> (5 - K)] = mine;
+    __syncwarp();
+    const float4 lo = *reinterpret_cast<const float4*>(sc);
+    const float4 hi = N == 8 ? *reinterpret_cast<const float4*>(sc + 4) : lo;
+    const float r[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
-  for (int q = 0; q < N; ++q)
-    if (S0 + q < 8) d[S0 + q] = __shfl_sync(0xffffffffu, mine, q << (5 - K));
+    for (int q = 0; q < N; ++q)
+      if (S0 + q < 8) d[S0 + q] = r[q];
+  } else {
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+      if (S0 + q < 8) d[S0 + q] = __shfl_sync(0xffffffffu, mine, q << (5 - K));
+  }
+}
+
+// Transposed butterfly over 8 per-lane binary64 partial sums: lane l returns the
+// warp sum of slot (l >> 2) & 7.  Each slot goes through the additions of
+// warp_sum's xor butterfly (16, 8, 4, 2, 1) with the same operand pairs, so the
+// result is bitwise the one warp_sum gives -- in 11 exchanges instead of 40.
+__device__ __forceinline__ double tsum8d(double (&e)[8], int l) {
+  {
+    const bool b = l & 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double send = b ? e[i] : e[i + 4], keep = b ? e[i + 4] : e[i];
+      e[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  {
+    const bool b = l & 8;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const double send = b ? e[i] : e[i + 2], keep = b ? e[i + 2] : e[i];
+      e[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  {
+    const bool b = l & 4;
+    const double send = b ? e[0] : e[1], keep = b ? e[1] : e[0];
+    e[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  e[0] += __shfl_xor_sync(0xffffffffu, e[0], 2);
+  e[0] += __shfl_xor_sync(0xffffffffu, e[0], 1);
+  return e[0];
+}
+
+// Same for 4 partial sums: lane l returns the warp sum of slot (l >> 3) & 3
+// (bitwise warp_sum's result), 6 exchanges instead of 20.
+__device__ __forceinline__ double tsum4d(double (&e)[4], int l) {
+  {
+    const bool b = l & 16;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const double send = b ? e[i] : e[i + 2], keep = b ? e[i + 2] : e[i];
+      e[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  {
+    const bool b = l & 8;
+    const double send = b ? e[0] : e[1], keep = b ? e[1] : e[0];
+    e[0] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int o = 4; o; o >>= 1) e[0] += __shfl_xor_sync(0xffffffffu, e[0], o);
+  return e[0];
 }
 
 #ifdef MLSB_PROBE
@@ -654,18 +721,33 @@ __device__ __forceinline__ F16 reduce16_core(F16 in, int l) {
     d[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
   }
   d[0] += __shfl_xor_sync(0xffffffffu, d[0], 1);
-  const float mine = d[0];  // value index (l >> 1) & 15
-#pragma unroll
-  for (int q = 0; q < 16; ++q) d[q] = __shfl_sync(0xffffffffu, mine, q << 1);
-  return in;
+  return in;  // d[0]: the sum of value (l >> 1) & 15
 }
-__device__ __forceinline__ void reduce16(float (&d)[16], int l) {
+// 16 + 2 partial sums per lane -> every lane gets all 18 sums: the transposed
+// butterfly for d, one more for the pair (e0, e1) (lanes < 16 end with e0, the
+// others with e1; the additions of warp_sum's butterfly), then the sums go
+// back to every lane through the warp's scratch `sc` (alternating between two
+// buffers from step to step) as five broadcast loads instead of 26 shuffles.
+__device__ __forceinline__ void reduce18(float (&d)[16], float& e0, float& e1, int l, float* sc) {
   F16 x;
 #pragma unroll
   for (int i = 0; i < 16; ++i) x.d[i] = d[i];
   x = reduce16_core(x, l);
+  const bool b4 = l & 16;
+  float e = (b4 ? e1 : e0) + __shfl_xor_sync(0xffffffffu, b4 ? e0 : e1, 16);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) d[i] = x.d[i];
+  for (int o = 8; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  if ((l & 1) == 0) sc[l >> 1] = x.d[0];
+  if ((l & 15) == 0) sc[16 + (l >> 4)] = e;
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 q = *reinterpret_cast<const float4*>(sc + 4 * i);
+    d[4 * i] = q.x, d[4 * i + 1] = q.y, d[4 * i + 2] = q.z, d[4 * i + 3] = q.w;
+  }
+  const float2 q2 = *reinterpret_cast<const float2*>(sc + 16);
+  e0 = q2.x;
+  e1 = q2.y;
 }
 
 // Reflector hand-off between warps: a ring of NVB reflector buffers guarded by
@@ -707,7 +789,7 @@ __device__ __forceinline__ void rq_crit(float2 (&br)[BT / 2][BS], const float (&
 template <int TO>
 __device__ __forceinline__ void rq_slot(float2 (&br)[BT / 2][BS], int m, int n, int p, int C, int w,
                                         int l, float* vbuf, float* tau2, float* TQ, uint64_t* full,
-                                        uint64_t* empty) {
+                                        uint64_t* empty, float* rsc) {
   if (NW * TO + NW - 1 < m || NW * TO >= m + p) return;  // no reflector rows in this slot
 #pragma unroll 1
   for (int wo = NW - 1; wo >= 0; --wo) {
@@ -750,9 +832,7 @@ __device__ __forceinline__ void rq_slot(float2 (&br)[BT / 2][BS], int m, int n, 
     float e0 = dd[8].x, e1 = dd[8].y;
     __syncwarp();
     if (l == 0) mbar_arrive(empty + b);
-    reduce16(d, l);
-    e0 = warp_sum(e0);
-    e1 = warp_sum(e1);
+    reduce18(d, e0, e1, l, rsc + 32 * (k & 1));
     const int jb = j & ~31;
     // rows above the reflector row are updated (the owner's row - 1 already
     // was); rows below it only give Gram entries.  tj == 0 means v = e_pc, whose
@@ -831,7 +911,7 @@ __device__ __forceinline__ void qr_crit(float2 (&ar)[RT][CS / 2], const float (&
 template <int SC>
 __device__ __forceinline__ void qr_slot(float2 (&ar)[RT][CS / 2], int m, int C, int kz, int w, int l,
                                         float* vbuf, float* tau1, float* TZ, uint64_t* full,
-                                        uint64_t* empty) {
+                                        uint64_t* empty, float* rsc) {
   constexpr int T0 = SC / 2, S0 = SC & ~1;
 #pragma unroll 1
   for (int jw = 0; jw < NW; ++jw) {
@@ -872,7 +952,7 @@ __device__ __forceinline__ void qr_slot(float2 (&ar)[RT][CS / 2], int m, int C, 
     __syncwarp();
     if (l == 0) mbar_arrive(empty + b);
     constexpr int NL = CS - S0 > 4 ? 8 : (CS - S0 > 2 ? 4 : 2);
-    reduce_live<(CS - NL > S0 ? S0 : CS - NL), NL>(d, l);
+    reduce_live<(CS - NL > S0 ? S0 : CS - NL), NL>(d, l, rsc + 32 * (j & 1));
     // slots S0..SC-1 hold finished columns of the current Gram block (c < j),
     // slot SC holds column j (w == jw) with finished columns below it and live
     // ones above, slots > SC hold live columns only.  The owner already updated
@@ -913,6 +993,61 @@ __device__ __forceinline__ void qr_slot(float2 (&ar)[RT][CS / 2], int m, int C, 
   }
 }
 
+// Residual sweep of the refinement loop for a compile-time shape with
+// lda = SM, ldb = SP (whole row slots on either side of the A/B boundary):
+// every load address is the lane's base pointer plus an immediate, every
+// bound and the A/B choice of a row slot are static.  Same sums in the same
+// order as the runtime-shape loop in the kernel; the four column sums of a
+// step share one transposed butterfly.
+template <int H, int SM, int SN, int SP>
+__device__ __forceinline__ void resid_fixed(const double* __restrict__ gA, const double* __restrict__ gB,
+                                            int l, int cg, double invA, double invB, const double* su,
+                                            const double* sw, double* dpart, double* cpart) {
+  constexpr int R = SM + SP, RB = H * RH;
+  static_assert(SM % 32 == 0 && SP % 32 == 0 && SN % (4 * CG) == 0, "whole slots");
+  const double* pa = gA + (RB + l) + size_t(cg) * SM;
+  const double* pb = gB + (RB + l - SM) + ptrdiff_t(cg) * SP;
+  double wv[RTH], racc[RTH];
+#pragma unroll
+  for (int t = 0; t < RTH; ++t) {
+    const int i = RB + l + 32 * t;
+    wv[t] = (RB + 32 * t < R) ? ((RB + 32 * t < SM) ? -sw[i] : sw[i]) : 0.0;
+    racc[t] = 0.0;
+  }
+#pragma unroll
+  for (int it = 0; it < SN / (4 * CG); ++it) {
+    double g[4][RTH];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int t = 0; t < RTH; ++t) {
+        const int co = (4 * it + q) * CG;  // column offset from cg
+        if (RB + 32 * t >= R) g[q][t] = 0.0;
+        else if (RB + 32 * t < SM) g[q][t] = __ldg(pa + 32 * t + co * SM);
+        else g[q][t] = __ldg(pb + 32 * t + co * SP);
+      }
+    double ca[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double xc = su[cg + (4 * it + q) * CG];
+      double cacc = 0.0;
+#pragma unroll
+      for (int t = 0; t < RTH; ++t) {
+        if (RB + 32 * t >= R) continue;
+        const double av = g[q][t] * ((RB + 32 * t < SM) ? invA : invB);
+        racc[t] = fma(av, xc, racc[t]);
+        cacc = fma(av, wv[t], cacc);
+      }
+      ca[q] = cacc;
+    }
+    const double cs = tsum4d(ca, l);  // lane 8 q: column cg + (4 it + q) CG
+    if ((l & 7) == 0) cpart[H * CMAX + cg + (4 * it + (l >> 3)) * CG] = cs;
+  }
+#pragma unroll
+  for (int t = 0; t < RTH; ++t)
+    if (RB + 32 * t < R) dpart[cg * RMAX + RB + l + 32 * t] = racc[t];
+}
+
 // -------------------------------------------------------------- kernel
 // SM, SN, SP > 0: the problem shape is a compile-time constant (BASELINE
 // config 4: 256 x 128 x 32), so every row/column bound, the live slot ranges
@@ -933,6 +1068,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   float* TZ = reinterpret_cast<float*>(smem + Ly.oTZ);
   float* TQ = reinterpret_cast<float*>(smem + Ly.oTQ);
   float* fpart = reinterpret_cast<float*>(smem + Ly.oU);           // [NW][RMAX]
+  float* rsc = fpart + 64 * w;  // this warp's reduction scratch during GRQ (2 x 32 floats)
   float* wbuf = fpart + NW * RMAX;                                  // [RMAX]
   float* vbuf = wbuf + RMAX;                                        // [NVB][RMAX]
   double* dpart = reinterpret_cast<double*>(smem + Ly.oU);         // [CG][RMAX]
@@ -998,19 +1134,25 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   double invA, invB;
   {
     double mx[3] = {0.0, 0.0, 0.0};
-    for (int j = w; j < C; j += NW) {
-      double g[RT];
+    // four columns (36 loads per lane) in flight per step: this first sweep
+    // reads the problem from HBM and is bound by the loads' latency
+    for (int j = w; j < C; j += 4 * NW) {
+      double g[4][RT];
 #pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int i = l + 32 * t;
-        g[t] = i < R ? gval(i, j) : 0.0;
-      }
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int i = l + 32 * t;
-        if (i < m) mx[0] = nanskip_max(mx[0], fabs(g[t]));
-        else mx[1] = nanskip_max(mx[1], fabs(g[t]));
-      }
+        for (int t = 0; t < RT; ++t) {
+          const int i = l + 32 * t, jj = j + q * NW;
+          g[q][t] = (i < R && jj < C) ? gval(i, jj) : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          const int i = l + 32 * t;
+          if (i < m) mx[0] = nanskip_max(mx[0], fabs(g[q][t]));
+          else mx[1] = nanskip_max(mx[1], fabs(g[q][t]));
+        }
     }
     for (int i = tid; i < m; i += NT) mx[2] = nanskip_max(mx[2], fabs(__ldg(gb + i)));
     block_max(mx, red, scal + S_RED0);
@@ -1046,22 +1188,27 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     // ------------------------------------------ scaled fp32 [A;B] -> smem (+ norms)
     {
       double ss[4] = {0.0, 0.0, 0.0, 0.0};
+      // four column slots per step (loads of the L2-resident copy all issued
+      // before use); the sums of squares keep their (slot, row) order
 #pragma unroll 1
-      for (int s = 0; s < CS; ++s) {
-        const int c = w + NW * s;
-        double g[RT];
+      for (int s0 = 0; s0 < CS; s0 += 4) {
+        double g[4][RT];
 #pragma unroll
-        for (int t = 0; t < RT; ++t) {
-          const int i = l + 32 * t;
-          g[t] = (c < C && i < R) ? gval(i, c) : 0.0;
-        }
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int t = 0; t < RT; ++t) {
-          const int i = l + 32 * t;
-          const double v = g[t] * (i < m ? invA : invB);
-          if (i < m) ss[0] = fma(v, v, ss[0]); else ss[1] = fma(v, v, ss[1]);
-          if (c < C && i < R) M[i + size_t(c) * ld] = float(v);
-        }
+          for (int t = 0; t < RT; ++t) {
+            const int i = l + 32 * t, c = w + NW * (s0 + q);
+            g[q][t] = (c < C && i < R) ? gval(i, c) : 0.0;
+          }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int t = 0; t < RT; ++t) {
+            const int i = l + 32 * t, c = w + NW * (s0 + q);
+            const double v = g[q][t] * (i < m ? invA : invB);
+            if (i < m) ss[0] = fma(v, v, ss[0]); else ss[1] = fma(v, v, ss[1]);
+            if (c < C && i < R) M[i + size_t(c) * ld] = float(v);
+          }
       }
       for (int i = tid; i < R; i += NT) {
         const double t = rinit[i];
@@ -1093,24 +1240,24 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
           const int i = w + NW * t, c = l + 32 * s;
           BR(t, s) = (i < R && c < C) ? M[i + size_t(c) * ld] : 0.f;
         }
-      rq_slot<17>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<16>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<15>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<14>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<13>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<12>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<11>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<10>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<9>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<8>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<7>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<6>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<5>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<4>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<3>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<2>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<1>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
-      rq_slot<0>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB);
+      rq_slot<17>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<16>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<15>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<14>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<13>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<12>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<11>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<10>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<9>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<8>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<7>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<6>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<5>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<4>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<3>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<2>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<1>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
+      rq_slot<0>(br, m, n, p, C, w, l, vbuf, tau2, TQ, mbar, mbar + NVB, rsc);
       __syncthreads();
 #pragma unroll
       for (int t = 0; t < BT; ++t)
@@ -1136,14 +1283,14 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
           const int i = l + 32 * t, c = w + NW * s;
           AR(t, s) = (i < R && c < C) ? M[i + size_t(c) * ld] : 0.f;
         }
-      qr_slot<0>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
-      qr_slot<1>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
-      qr_slot<2>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
-      qr_slot<3>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
-      qr_slot<4>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
-      qr_slot<5>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
-      qr_slot<6>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
-      qr_slot<7>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB);
+      qr_slot<0>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB, rsc);
+      qr_slot<1>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB, rsc);
+      qr_slot<2>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB, rsc);
+      qr_slot<3>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB, rsc);
+      qr_slot<4>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB, rsc);
+      qr_slot<5>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB, rsc);
+      qr_slot<6>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB, rsc);
+      qr_slot<7>(ar, m, C, kz, w, l, vbuf, tau1, TZ, mbar + 2 * NVB, mbar + 3 * NVB, rsc);
       __syncthreads();
       stamp(3);
 #pragma unroll
@@ -1327,7 +1474,10 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     const int k = n - p;
     for (pass = 1; pass <= a.maxit; ++pass) {
       // ---- residual: rows f = [b - r; d] - M x ; cols f3 = M^T [-r; v]
-      {
+      if constexpr (SM > 0 && SM % 32 == 0 && SP % 32 == 0 && SN % (4 * CG) == 0) {
+        if (w < CG) resid_fixed<0, SM, SN, SP>(gA, gB, l, w, invA, invB, su, sw, dpart, cpart);
+        else resid_fixed<1, SM, SN, SP>(gA, gB, l, w - CG, invA, invB, su, sw, dpart, cpart);
+      } else {
         const int cg = w & (CG - 1), h = w >> 3;
         double wv[RTH], racc[RTH];
 #pragma unroll
@@ -1398,14 +1548,35 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
           nv[2] = fma(f, f, nv[2]);
           nv[5] = fma(s, s, nv[5]);
         }
-        block_sum(nv, red, scal + S_RED0);
-        if (LOWS) block_max(mx, red, scal + S_SIG);
+        // one fused block reduction (six sums + the max), bitwise the sums of
+        // block_sum: per warp a transposed butterfly, then warp 0 reduces the
+        // 16 warp results the same way, takes the six square roots on six lanes
+        // and decides -- two CTA barriers per stop test instead of five
+        double e8[8] = {nv[0], nv[1], nv[2], nv[3], nv[4], nv[5], 0.0, 0.0};
+        const double ws = tsum8d(e8, l);
+        const double wm = LOWS ? warp_max(mx[0]) : 0.0;
+        if ((l & 3) == 0) red[w * 8 + (l >> 2)] = ws;
+        if (l == 0) red[NW * 8 + w] = wm;
+      }
+      __syncthreads();
+      double g1 = 0, g2 = 0, g3 = 0, nr = 0, nv2 = 0, nx = 0;
+      if (w == 0) {
+        double e8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) e8[q] = l < NW ? red[l * 8 + q] : 0.0;
+        const double rt = sqrt(tsum8d(e8, l));  // lane 4 q: slot q
+        g1 = __shfl_sync(0xffffffffu, rt, 0);
+        g2 = __shfl_sync(0xffffffffu, rt, 4);
+        g3 = __shfl_sync(0xffffffffu, rt, 8);
+        nr = __shfl_sync(0xffffffffu, rt, 12);
+        nv2 = __shfl_sync(0xffffffffu, rt, 16);
+        nx = __shfl_sync(0xffffffffu, rt, 20);
+        if (LOWS) {
+          const double mm = warp_max(l < NW ? red[NW * 8 + l] : 0.0);
+          if (l == 0) scal[S_SIG] = mm;
+        }
       }
       if (tid == 0) {
-        const double g1 = sqrt(scal[S_RED0]), g2 = sqrt(scal[S_RED0 + 1]),
-                     g3 = sqrt(scal[S_RED0 + 2]);
-        const double nr = sqrt(scal[S_RED0 + 3]), nv2 = sqrt(scal[S_RED0 + 4]),
-                     nx = sqrt(scal[S_RED0 + 5]);
         const double d1 = nb + nr + nA * nx, d2 = nd + nB * nx, d3 = nA * nr + nB * nv2;
         if (hist) {
           hist[(pass - 1) * 3 + 0] = g1 * cb;
@@ -1570,8 +1741,10 @@ static cudaError_t launch_ct(const TileArgs& a, cudaStream_t st) {
   static const int opts = getenv("MLSB_REG_OPTS") ? atoi(getenv("MLSB_REG_OPTS")) : 0;
   TileArgs a2 = a;
   a2.opts = opts;
-  auto kern = (a.m == 256 && a.n == 128 && a.p == 32) ? lse_reg_kernel<CT, 256, 128, 32>
-                                                      : lse_reg_kernel<CT>;
+  // the shape-specialised kernel also assumes packed problems (lda = m, ldb = p)
+  auto kern = (a.m == 256 && a.n == 128 && a.p == 32 && a.lda == 256 && a.ldb == 32)
+                  ? lse_reg_kernel<CT, 256, 128, 32>
+                  : lse_reg_kernel<CT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(L.total));
   if (e != cudaSuccess) return e;

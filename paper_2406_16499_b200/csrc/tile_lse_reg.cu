@@ -170,18 +170,19 @@ __device__ __forceinline__ double tsum8d(double (&e)[8], int l) {
 
 // Same for 4 partial sums: lane l returns the warp sum of slot (l >> 3) & 3
 // (bitwise warp_sum's result), 6 exchanges instead of 20.
-__device__ __forceinline__ double tsum4d(double (&e)[4], int l) {
+template <class T>
+__device__ __forceinline__ T tsum4d(T (&e)[4], int l) {
   {
     const bool b = l & 16;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      const double send = b ? e[i] : e[i + 2], keep = b ? e[i + 2] : e[i];
+      const T send = b ? e[i] : e[i + 2], keep = b ? e[i + 2] : e[i];
       e[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
   }
   {
     const bool b = l & 8;
-    const double send = b ? e[0] : e[1], keep = b ? e[1] : e[0];
+    const T send = b ? e[0] : e[1], keep = b ? e[1] : e[0];
     e[0] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
   }
 #pragma unroll
@@ -492,17 +493,26 @@ __device__ void gemv_rows(const float* M, int ld, int r0, int rows, int c0, int 
 template <class CT, bool LOWER_MASK>
 __device__ void gemv_cols(const float* M, int ld, int r0, int rows, int c0, int cols, const CT* x,
                           CT* y, int wfirst, int nwarps, int w, int l) {
-  for (int j = w - wfirst; j < cols; j += nwarps) {
-    const float* colp = M + size_t(c0 + j) * ld + r0;
-    int imax = rows;
-    if (LOWER_MASK) {
-      const int lim = (c0 + j) - r0 + 1;  // rows r0+i <= c0+j
-      imax = lim < rows ? (lim > 0 ? lim : 0) : rows;
+  // four columns per step: independent accumulation chains and one transposed
+  // butterfly for the four sums (bitwise the per-column warp_sum)
+  for (int j0 = 4 * (w - wfirst); j0 < cols; j0 += 4 * nwarps) {
+    CT acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q < cols ? j0 + q : cols - 1;
+      const float* colp = M + size_t(c0 + j) * ld + r0;
+      int imax = rows;
+      if (LOWER_MASK) {
+        const int lim = (c0 + j) - r0 + 1;  // rows r0+i <= c0+j
+        imax = lim < rows ? (lim > 0 ? lim : 0) : rows;
+      }
+      CT a = CT(0);
+      for (int i = l; i < imax; i += 32) a += CT(colp[i]) * x[i];
+      acc[q] = a;
     }
-    CT acc = CT(0);
-    for (int i = l; i < imax; i += 32) acc += CT(colp[i]) * x[i];
-    acc = warp_sum(acc);
-    if (l == 0) y[j] = acc;
+    const CT sum = tsum4d(acc, l);
+    const int jq = j0 + (l >> 3);
+    if ((l & 7) == 0 && jq < cols) y[jq] = sum;
   }
 }
 
@@ -1048,6 +1058,68 @@ __device__ __forceinline__ void resid_fixed(const double* __restrict__ gA, const
     if (RB + 32 * t < R) dpart[cg * RMAX + RB + l + 32 * t] = racc[t];
 }
 
+// Fixed-shape forms of the other sweeps over the fp64 inputs (same sums in
+// the same order as the runtime-shape loops in the kernel).
+// r_f = b_f - A_f x_f: fp32 row sums of the A rows of row half H
+template <int H, int SM, int SN>
+__device__ __forceinline__ void init_resid_fixed(const double* __restrict__ gA, int l, int cg, double invA,
+                                                 const float* y, float* fpart) {
+  constexpr int RB = H * RH;
+  const double* pa = gA + (RB + l) + size_t(cg) * SM;
+  float racc[RTH];
+#pragma unroll
+  for (int t = 0; t < RTH; ++t) racc[t] = 0.f;
+#pragma unroll
+  for (int it = 0; it < SN / (4 * CG); ++it) {
+    double g[4][RTH];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int t = 0; t < RTH; ++t)
+        g[q][t] = (RB + 32 * t < SM) ? __ldg(pa + 32 * t + (4 * it + q) * CG * SM) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float xc = y[cg + (4 * it + q) * CG];
+#pragma unroll
+      for (int t = 0; t < RTH; ++t)
+        if (RB + 32 * t < SM) racc[t] = fmaf(xc, float(g[q][t] * invA), racc[t]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < RTH; ++t)
+    if (RB + 32 * t < SM) fpart[cg * RMAX + RB + l + 32 * t] = racc[t];
+}
+// g = A^T r: fp64 column sums over the A rows of row half H
+template <int H, int SM, int SN>
+__device__ __forceinline__ void atr_fixed(const double* __restrict__ gA, int l, int cg, double invA,
+                                          const double* sw, double* cpart) {
+  constexpr int RB = H * RH;
+  const double* pa = gA + (RB + l) + size_t(cg) * SM;
+  double wv[RTH];
+#pragma unroll
+  for (int t = 0; t < RTH; ++t) wv[t] = (RB + 32 * t < SM) ? sw[RB + l + 32 * t] : 0.0;
+#pragma unroll
+  for (int it = 0; it < SN / (4 * CG); ++it) {
+    double g[4][RTH];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int t = 0; t < RTH; ++t)
+        g[q][t] = (RB + 32 * t < SM) ? __ldg(pa + 32 * t + (4 * it + q) * CG * SM) : 0.0;
+    double ca[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t < RTH; ++t)
+        if (RB + 32 * t < SM) acc = fma(g[q][t] * invA, wv[t], acc);
+      ca[q] = acc;
+    }
+    const double cs = tsum4d(ca, l);
+    if ((l & 7) == 0) cpart[H * CMAX + cg + (4 * it + (l >> 3)) * CG] = cs;
+  }
+}
+
 // -------------------------------------------------------------- kernel
 // SM, SN, SP > 0: the problem shape is a compile-time constant (BASELINE
 // config 4: 256 x 128 x 32), so every row/column bound, the live slot ranges
@@ -1061,6 +1133,10 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   const Layout Ly = make_layout(m, n, p, sizeof(CT));
   const int R = Ly.R, C = Ly.C, ld = Ly.ld, kz = Ly.kz;
   constexpr bool LOWS = sizeof(CT) == 4;
+  // compile-time shape with whole 32-row slots on either side of the A/B
+  // boundary and packed problems (lda = m, ldb = p; checked at launch): the
+  // sweeps over the fp64 inputs address them as lane base + immediate
+  constexpr bool FIXED = SM > 0 && SM % 32 == 0 && SP % 32 == 0 && SN % (4 * CG) == 0 && SN % (4 * NW) == 0;
 
   float* M = reinterpret_cast<float*>(smem + Ly.oM);
   float* tau1 = reinterpret_cast<float*>(smem + Ly.oTau1);
@@ -1143,7 +1219,13 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
 #pragma unroll
         for (int t = 0; t < RT; ++t) {
           const int i = l + 32 * t, jj = j + q * NW;
-          g[q][t] = (i < R && jj < C) ? gval(i, jj) : 0.0;
+          if constexpr (FIXED) {  // lane base + (loop-invariant) offset, static A/B slots
+            if (32 * t < SM) g[q][t] = __ldg(gA + l + size_t(w) * SM + 32 * t + size_t(jj - w) * SM);
+            else if (32 * t < SM + SP) g[q][t] = __ldg(gB + l + size_t(w) * SP + (32 * t - SM) + size_t(jj - w) * SP);
+            else g[q][t] = 0.0;
+          } else {
+            g[q][t] = (i < R && jj < C) ? gval(i, jj) : 0.0;
+          }
         }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -1198,7 +1280,14 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
 #pragma unroll
           for (int t = 0; t < RT; ++t) {
             const int i = l + 32 * t, c = w + NW * (s0 + q);
-            g[q][t] = (c < C && i < R) ? gval(i, c) : 0.0;
+            if constexpr (FIXED) {
+              if (32 * t < SM) g[q][t] = __ldg(gA + l + size_t(w) * SM + 32 * t + size_t(NW * (s0 + q)) * SM);
+              else if (32 * t < SM + SP)
+                g[q][t] = __ldg(gB + l + size_t(w) * SP + (32 * t - SM) + size_t(NW * (s0 + q)) * SP);
+              else g[q][t] = 0.0;
+            } else {
+              g[q][t] = (c < C && i < R) ? gval(i, c) : 0.0;
+            }
           }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -1369,7 +1458,19 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     __syncthreads();
     if (iflag[0]) goto finish;
     // r_f = b_f - A_f x_f with A_f = fl32(A / s_A) streamed again (row sums, fp32)
-    {
+    if constexpr (FIXED) {
+      if (w < CG) init_resid_fixed<0, SM, SN>(gA, l, w, invA, y, fpart);
+      else init_resid_fixed<1, SM, SN>(gA, l, w - CG, invA, y, fpart);
+      __syncthreads();
+      for (int i = tid; i < m; i += NT) {
+        float acc = 0.f;
+#pragma unroll
+        for (int g2 = 0; g2 < CG; ++g2) acc += fpart[g2 * RMAX + i];
+        sw[i] = double(bf[i] - acc);
+      }
+      for (int j = tid; j < n; j += NT) su[j] = double(y[j]);
+      __syncthreads();
+    } else {
       const int cg = w & (CG - 1), h = w >> 3;
       float racc[RTH];
 #pragma unroll
@@ -1409,6 +1510,10 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     // solve_v (lse.hpp:156-165): g = A^T r at fp64, sigma, Q g, R^T v = g(n-p:n)
     {
       const int cg = w & (CG - 1), h = w >> 3;
+      if constexpr (FIXED) {
+        if (w < CG) atr_fixed<0, SM, SN>(gA, l, w, invA, sw, cpart);
+        else atr_fixed<1, SM, SN>(gA, l, w - CG, invA, sw, cpart);
+      } else {
       double wv[RTH];
 #pragma unroll
       for (int t = 0; t < RTH; ++t) {
@@ -1433,6 +1538,7 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
           const int cc = c0 + q * CG;
           if (l == 0 && cc < n) cpart[h * CMAX + cc] = acc;
         }
+      }
       }
       __syncthreads();
       for (int j = tid; j < n; j += NT) cout[j] = cpart[j] + cpart[CMAX + j];
@@ -1631,26 +1737,31 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
         z_apply_mw<CT>(M, ld, kz, m, TZ, true, wv, partZ, wsc, Grp{w, ZG, l, 1});  // w = Z^T f1
         if (pass == 1) stampw(16, 0);
       } else if (w < ZG + QG) {
-        q_apply_mw<CT>(M, ld, p, m, n - p, n, TQ, false, u, partQ, wsc, Grp{w - ZG, QG, l, 2});  // u = Q f3
+        // u = Q f3, then (one warp of the group) T11^T q1 = u1 -- both done
+        // while the Z group is still in its four WY blocks
+        const Grp g{w - ZG, QG, l, 2};
+        q_apply_mw<CT>(M, ld, p, m, n - p, n, TQ, false, u, partQ, wsc, g);
         if (pass == 1) stampw(17, ZG);
-      } else if (w == ZG + QG) {
-        trsv_up<CT>(M, ld, m, n - p, p, rinvR, y2, l);
+        g.sync();
+        if (g.gw == 0) {
+          for (int i = l; i < k; i += 32) q1[i] = u[i];
+          __syncwarp();
+          trsv_upt<CT>(M, ld, 0, 0, k, rinvT, q1, l);
+          if (pass == 1) stampw(23, ZG);
+        }
+      } else {
+        // the remaining warps: y2 = R^-1 f2, then T12 y2 and T22 y2
+        constexpr int NG = NW - ZG - QG;
+        const Grp g{w - ZG - QG, NG, l, 3};
+        if (g.gw == 0) trsv_up<CT>(M, ld, m, n - p, p, rinvR, y2, l);
         if (pass == 1) stampw(18, ZG + QG);
+        g.sync();
+        gemv_rows<CT, false>(M, ld, 0, k, k, p, y2, t4, tid - 32 * (ZG + QG), 32 * NG);
+        gemv_rows<CT, true>(M, ld, k, m - k, k, p, y2, t4 + k, tid - 32 * (ZG + QG), 32 * NG);
+        if (pass == 1) stampw(24, ZG + QG);
       }
       __syncthreads();
       if (pass == 1) stamp(8);
-      if (iflag[0]) break;
-      if (w == 0) {
-        for (int i = l; i < k; i += 32) q1[i] = u[i];
-        __syncwarp();
-        trsv_upt<CT>(M, ld, 0, 0, k, rinvT, q1, l);
-        if (pass == 1) stampw(23, 0);
-      } else {
-        gemv_rows<CT, false>(M, ld, 0, k, k, p, y2, t4, tid - 32, NT - 32);
-        gemv_rows<CT, true>(M, ld, k, m - k, k, p, y2, t4 + k, tid - 32, NT - 32);
-        if (pass == 1) stampw(24, 1);
-      }
-      __syncthreads();
       if (pass == 1) stamp(9);
       if (iflag[0]) break;
       for (int i = tid; i < m; i += NT) {
@@ -1673,23 +1784,25 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
         if (pass == 1) stampw(20, 0);
       } else if (w < NW - ZG) {
         // s = T12^T q1 + (T22^T q2 - u2)  (q = wv)
+        // ... then (one warp of the group) R^T dv = s, while the Z group is
+        // still in its four WY blocks
         constexpr int NG = NW - ZG - QG;
+        const Grp g{w - QG, NG, l, 3};
         gemv_cols<CT, false>(M, ld, 0, k, k, p, wv, t4, QG, NG, w, l);
         gemv_cols<CT, true>(M, ld, k, m - k, k, p, wv + k, q1, QG, NG, w, l);
         if (pass == 1) stampw(21, QG);
+        g.sync();
+        if (g.gw == 0) {
+          for (int i = l; i < p; i += 32) t4[i] = t4[i] + (q1[i] - u[k + i]);
+          __syncwarp();
+          trsv_upt<CT>(M, ld, m, n - p, p, rinvR, t4, l);
+        }
       } else {
         z_apply_mw<CT>(M, ld, kz, m, TZ, false, dr, partZ, wsc, Grp{w - (NW - ZG), ZG, l, 1});  // dr = Z q
         if (pass == 1) stampw(22, NW - ZG);
       }
       __syncthreads();
       if (pass == 1) stamp(10);
-      if (iflag[0]) break;
-      if (w == 1) {
-        for (int i = l; i < p; i += 32) t4[i] = t4[i] + (q1[i] - u[k + i]);
-        __syncwarp();
-        trsv_upt<CT>(M, ld, m, n - p, p, rinvR, t4, l);
-      }
-      __syncthreads();
       if (iflag[0]) break;
       int bad = 0;
       for (int i = tid; i < m; i += NT) {

@@ -279,10 +279,18 @@ __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, c
   const int pk = (g.gw == 0 && l == 0 && tr) ? 8 * (i0 >> 5) : -1;
   if (pk >= 0) PROBE1(pk);
   float v[32];
+  // full block and every entry of this warp strictly inside the reflectors'
+  // stored part (warp-uniform): plain loads, no triangle / range masks
+  const bool plain = kb == 32 && vf.plain(32 * g.gw, i0, i1);
+  if (plain) {
 #pragma unroll
-  for (int q = 0; q < 32; ++q) {
-    const float vq = vf(i, q);  // branch-free (clamped) load
-    v[q] = (act && q < kb) ? vq : 0.f;
+    for (int q = 0; q < 32; ++q) v[q] = vf.raw(i, q);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const float vq = vf(i, q);  // branch-free (clamped) load
+      v[q] = (act && q < kb) ? vq : 0.f;
+    }
   }
   const CT xi = act ? x[i] : CT(0);
   part[32 * g.gw + l] = tsum32(v, xi, l);
@@ -296,14 +304,26 @@ __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, c
   ws[l] = y;
   __syncwarp();
   CT z0 = CT(0), z1 = CT(0);
+  if (kb == 32) {
+    // build_T stores the whole 32 x 32 block with exact zeros below the
+    // diagonal: the triangle mask is in the data
 #pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const CT yk = ws[k];
-    const bool use = k < kb && (tr ? k <= l : k >= l);
-    const float tv = Tb[tr ? k + TLD * l : l + TLD * k];
-    const float t = use ? tv : 0.f;
-    if (k & 1) z1 += CT(t) * yk;
-    else z0 += CT(t) * yk;
+    for (int k = 0; k < 32; ++k) {
+      const CT yk = ws[k];
+      const float t = Tb[tr ? k + TLD * l : l + TLD * k];
+      if (k & 1) z1 += CT(t) * yk;
+      else z0 += CT(t) * yk;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const CT yk = ws[k];
+      const bool use = k < kb && (tr ? k <= l : k >= l);
+      const float tv = Tb[tr ? k + TLD * l : l + TLD * k];
+      const float t = use ? tv : 0.f;
+      if (k & 1) z1 += CT(t) * yk;
+      else z0 += CT(t) * yk;
+    }
   }
   const CT z = l < kb ? z0 + z1 : CT(0);
   if (pk >= 0) PROBE1(pk + 3);
@@ -333,6 +353,11 @@ struct ZV {
     const float mv = M[rr + size_t(j0 + q) * ld];
     return d > q ? mv : (d == q ? 1.f : 0.f);
   }
+  // rows r0 .. r0+31 all below the block's unit diagonals and inside [i0, i1)
+  __device__ __forceinline__ bool plain(int r0, int i0, int i1) const {
+    return r0 >= j0 + 32 && r0 >= i0 && r0 + 32 <= i1;
+  }
+  __device__ __forceinline__ float raw(int r, int q) const { return M[r + size_t(j0 + q) * ld]; }
 };
 // RQ (Q) reflectors in rows rtop + j: entries at columns c < ptop + j, unit at
 // c = ptop + j; entry index = column
@@ -345,6 +370,11 @@ struct QV {
     const float mv = M[(row0 + q) + size_t(cc) * ld];
     return c < pc ? mv : (c == pc ? 1.f : 0.f);
   }
+  // columns c0 .. c0+31 all left of the block's unit entries and inside [i0, i1)
+  __device__ __forceinline__ bool plain(int c0, int i0, int i1) const {
+    return c0 + 32 <= pc0 && c0 >= i0 && c0 + 32 <= i1;
+  }
+  __device__ __forceinline__ float raw(int c, int q) const { return M[(row0 + q) + size_t(c) * ld]; }
 };
 
 // Z x (herm = false: last block first, T) or Z^T x (first block first, T^T);
@@ -411,7 +441,12 @@ __device__ void trsv_up(const float* M, int ld, int r0, int c0, int k, const CT*
     for (int r = l; r < i0; r += 32) {
       CT acc = CT(0);
       const float* rowp = M + (r0 + r) + size_t(c0 + i0) * ld;
-      for (int q = 0; q < bs; ++q) acc += CT(rowp[size_t(q) * ld]) * x[i0 + q];
+      if (bs == 32) {  // full block: the 64 loads issue ahead of the (same, sequential) sum
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc += CT(rowp[size_t(q) * ld]) * x[i0 + q];
+      } else {
+        for (int q = 0; q < bs; ++q) acc += CT(rowp[size_t(q) * ld]) * x[i0 + q];
+      }
       x[r] -= acc;
     }
     __syncwarp();
@@ -447,7 +482,12 @@ __device__ void trsv_upt(const float* M, int ld, int r0, int c0, int k, const CT
     for (int r = i1 + l; r < k; r += 32) {
       CT acc = CT(0);
       const float* colp = M + (r0 + i0) + size_t(c0 + r) * ld;
-      for (int q = 0; q < bs; ++q) acc += CT(colp[q]) * x[i0 + q];
+      if (bs == 32) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc += CT(colp[q]) * x[i0 + q];
+      } else {
+        for (int q = 0; q < bs; ++q) acc += CT(colp[q]) * x[i0 + q];
+      }
       x[r] -= acc;
     }
     __syncwarp();

@@ -1671,8 +1671,10 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
         rout[i] = (i < m ? rinit[i] - sw[i] : rinit[i]) - acc;
       }
       for (int j = tid; j < n; j += NT) cout[j] = cpart[j] + cpart[CMAX + j];
-      __syncthreads();
-      if (pass == 1) {
+      // no CTA barrier here: the norms below read the entries of rout / cout
+      // this thread has just written (same index mapping)
+      if (pass == 1 && g_dump != nullptr) {
+        __syncthreads();
         dump_d(pid, 93200, rout, R, tid);
         dump_d(pid, 94000, cout, C, tid);
       }

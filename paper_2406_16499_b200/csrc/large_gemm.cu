@@ -245,11 +245,16 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
       }
     }
   };
-  float acc[8][8];
+  // accumulators as row pairs (rows 2a', 2a'+1 of one column): the inner
+  // product is packed FFMA2 (fma.rn.f32x2: two independent binary32 FMAs per
+  // instruction, the operands and rounding of the fmaf each replaces), which
+  // halves the issue slots of the 64 FMAs of a kk step
+  float2 acc2[4][8];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+    for (int b = 0; b < 8; ++b) acc2[a][b] = make_float2(0.f, 0.f);
+#define ACC(a, b) ((((a) & 1) != 0) ? acc2[(a) >> 1][b].y : acc2[(a) >> 1][b].x)
   auto store_a = [&](int buf, int part) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -284,12 +289,13 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
     const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + tr * 4]);
     const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tc * 4]);
     const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tc * 4]);
-    const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float2 ap[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
+                          make_float2(a1.z, a1.w)};
     const float bf[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(af[a], bf[b], acc[a][b]);
+      for (int b = 0; b < 8; ++b) acc2[a][b] = __ffma2_rn(ap[a], make_float2(bf[b], bf[b]), acc2[a][b]);
   };
 
 
@@ -345,8 +351,8 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
         const int gj = j0 + (b < 4 ? tc * 4 + b : 64 + tc * 4 + b - 4);
-        float4 v = make_float4(alpha * acc[4 * h][b], alpha * acc[4 * h + 1][b], alpha * acc[4 * h + 2][b],
-                               alpha * acc[4 * h + 3][b]);
+        float4 v = make_float4(alpha * ACC(4 * h, b), alpha * ACC(4 * h + 1, b), alpha * ACC(4 * h + 2, b),
+                               alpha * ACC(4 * h + 3, b));
         if (beta != 0.f)
           v.x = fmaf(beta, o[b].x, v.x), v.y = fmaf(beta, o[b].y, v.y), v.z = fmaf(beta, o[b].z, v.z),
           v.w = fmaf(beta, o[b].w, v.w);
@@ -364,8 +370,8 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
     for (int h = 0; h < 2; ++h) {
       const int gi = i0 + h * 64 + tr * 4;
       if (cvec && gi + 3 < M) {
-        float4 v = make_float4(alpha * acc[4 * h][b], alpha * acc[4 * h + 1][b], alpha * acc[4 * h + 2][b],
-                               alpha * acc[4 * h + 3][b]);
+        float4 v = make_float4(alpha * ACC(4 * h, b), alpha * ACC(4 * h + 1, b), alpha * ACC(4 * h + 2, b),
+                               alpha * ACC(4 * h + 3, b));
         if (beta != 0.f) {
           const float4 o = *reinterpret_cast<const float4*>(cj + gi);
           v.x = fmaf(beta, o.x, v.x), v.y = fmaf(beta, o.y, v.y), v.z = fmaf(beta, o.z, v.z), v.w = fmaf(beta, o.w, v.w);
@@ -375,7 +381,7 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           if (gi + t >= M) continue;
-          float v = alpha * acc[4 * h + t][b];
+          float v = alpha * ACC(4 * h + t, b);
           if (beta != 0.f) v = fmaf(beta, cj[gi + t], v);
           cj[gi + t] = v;
         }
@@ -383,6 +389,7 @@ __device__ __forceinline__ void sgemm128_tile(int M, int N, int K, float alpha, 
     }
   }
 }
+#undef ACC
 
 // Persistent form: the grid may be smaller than the tile count (gm x gn x gz),
 // each CTA walking tiles with a stride, so a trailing update can leave SMs

@@ -271,11 +271,33 @@ __device__ __forceinline__ CT tsum32(const float (&v)[32], CT xv, int l) {
 // V stays in registers between the two products; V^T x is a transposed warp
 // reduction plus a fixed-order sum over the group's warps (`part`,
 // double-buffered by the caller, so one barrier per block).
+// the warp's 32-entry scratch as broadcast 16-byte loads
+__device__ __forceinline__ void load32(const float* ws, float (&o)[32]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float4 q = *reinterpret_cast<const float4*>(ws + 4 * k);
+    o[4 * k] = q.x, o[4 * k + 1] = q.y, o[4 * k + 2] = q.z, o[4 * k + 3] = q.w;
+  }
+}
+__device__ __forceinline__ void load32(const double* ws, double (&o)[32]) {
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const double2 q = *reinterpret_cast<const double2*>(ws + 2 * k);
+    o[2 * k] = q.x, o[2 * k + 1] = q.y;
+  }
+}
 template <class CT, class VF>
 __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, const float* Tb,
                                          bool tr, CT* x, CT* part, CT* ws, const Grp& g) {
   const int l = g.l, i = 32 * g.gw + l;
   const bool act = i >= i0 && i < i1;
+  if (32 * g.gw + 32 <= i0 || 32 * g.gw >= i1) {
+    // no entry of this warp is touched by the block (warp-uniform): it only
+    // contributes its zero partial and the group barrier
+    part[32 * g.gw + l] = CT(0);
+    g.sync();
+    return;
+  }
   const int pk = (g.gw == 0 && l == 0 && tr) ? 8 * (i0 >> 5) : -1;
   if (pk >= 0) PROBE1(pk);
   float v[32];
@@ -307,9 +329,11 @@ __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, c
   if (kb == 32) {
     // build_T stores the whole 32 x 32 block with exact zeros below the
     // diagonal: the triangle mask is in the data
+    CT yv[32];
+    load32(ws, yv);
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
-      const CT yk = ws[k];
+      const CT yk = yv[k];
       const float t = Tb[tr ? k + TLD * l : l + TLD * k];
       if (k & 1) z1 += CT(t) * yk;
       else z0 += CT(t) * yk;
@@ -331,10 +355,14 @@ __device__ __forceinline__ void wy_block(const VF& vf, int i0, int i1, int kb, c
   ws[l] = z;
   __syncwarp();
   CT a0 = CT(0), a1 = CT(0);
+  {
+    CT zv[32];
+    load32(ws, zv);
 #pragma unroll
-  for (int q = 0; q < 32; q += 2) {
-    a0 += CT(v[q]) * ws[q];
-    a1 += CT(v[q + 1]) * ws[q + 1];
+    for (int q = 0; q < 32; q += 2) {
+      a0 += CT(v[q]) * zv[q];
+      a1 += CT(v[q + 1]) * zv[q + 1];
+    }
   }
   __syncwarp();  // ws is rewritten by the next block
   if (act) x[i] = xi - (a0 + a1);

@@ -38,6 +38,7 @@ struct TileArgs {
   void* gws;         // per-problem factor workspace in global memory, or null (shared memory)
   unsigned long long* stamps;  // debug: globaltimer stamps of problem 0 (MLSB_DEBUG_STAMPS), or null
   int opts = 0;                // kernel variant bits (A/B switches), 0 = product configuration
+  int opts2 = 0;               // second A/B parameter
 };
 
 // shared-memory bytes the tile solver needs for this shape/precision

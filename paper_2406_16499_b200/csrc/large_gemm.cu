@@ -527,11 +527,12 @@ static void launch128(bool ha, bool hb, dim3 tiles, int M, int N, int K, float a
   const int nt = int(tiles.x * tiles.y * tiles.z);
   const int grid = g_gemm_cta_cap > 0 ? std::min(nt, g_gemm_cta_cap) : nt;
   const int gm = int(tiles.x), gn = int(tiles.y), gz = int(tiles.z);
-  // k-tile per operand layout: the NT form (B transposed, the RQ trailing
-  // update) spills at BK = 32 and is fastest at 16; the others at 32
-  // (scripts/dbg/gemm_rate.py at the C3 shapes)
+  // k-tile: 32 for every operand layout since the FFMA2 inner product (the NT
+  // form, the RQ trailing update, was faster at 16 before: now 0.583 vs 0.567
+  // of the FP32 peak at the C3 shape; MLSB_GEMM_NT16=1 restores it)
   static const bool bk16 = getenv("MLSB_GEMM_BK16") != nullptr;
-  if (bk16 || (!ha && hb))
+  static const bool nt16 = getenv("MLSB_GEMM_NT16") != nullptr;
+  if (bk16 || (!ha && hb && nt16))
     launch128_bk<VEC, 16>(ha, hb, grid, gm, gn, gz, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, st);
   else
     launch128_bk<VEC, GBK>(ha, hb, grid, gm, gn, gz, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, sstr, st);

@@ -1949,7 +1949,10 @@ static cudaError_t launch_ct(const TileArgs& a, cudaStream_t st) {
     return sms * 19 / 20;
   }();
   TileArgs a2 = a;
-  a2.opts = opts;
+  // the bulk prefetch needs 16-byte aligned problem bases
+  const bool pf_ok = reinterpret_cast<uintptr_t>(a.A) % 16 == 0 && reinterpret_cast<uintptr_t>(a.B) % 16 == 0 &&
+                    (a.sA % 2) == 0 && (a.sB % 2) == 0;
+  a2.opts = pf_ok ? opts : 0;
   a2.opts2 = opts2;
   // the shape-specialised kernel also assumes packed problems (lda = m, ldb = p)
   auto kern = (a.m == 256 && a.n == 128 && a.p == 32 && a.lda == 256 && a.ldb == 32)

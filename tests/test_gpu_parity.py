@@ -305,3 +305,23 @@ def test_batched_bitwise_reproducible(gpu, shape):
     if shape == (256, 128, 32):
         h = P.mplse_batched(A.cpu().numpy(), B.cpu().numpy(), b.cpu().numpy(), d.cpu().numpy())
         assert np.array_equal(h.x, o1.x.cpu().numpy())
+
+
+def test_batched_c4_shape_unaligned_base(gpu):
+    """The C4 kernel's L2 bulk prefetch needs 16-byte aligned problem bases: a batch
+    whose A starts 8 bytes into an allocation must still run (prefetch off) and
+    give bitwise the aligned run's results."""
+    import torch
+
+    P = gpu
+    nb, m, n, p = 600, 256, 128, 32
+    A, B, b, d, _ = G.lse_batch_torch(nb, m, n, p, seed=1000, device="cuda")
+    ref = P.mplse_batched(A, B, b, d)
+    buf = torch.empty(nb * m * n + 1, dtype=torch.float64, device="cuda")
+    Au = buf[1:].view(nb, n, m).transpose(1, 2)
+    assert Au.data_ptr() % 16 == 8 and Au.stride() == A.stride()
+    Au.copy_(A)
+    out = P.mplse_batched(Au, B, b, d)
+    torch.cuda.synchronize()
+    for f in ("x", "r", "v", "iterations", "status"):
+        assert np.array_equal(getattr(ref, f).cpu().numpy(), getattr(out, f).cpu().numpy()), f

@@ -1249,14 +1249,14 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
   uint64_t t_last = 0;
   double ph[6] = {0, 0, 0, 0, 0, 0};
   auto lap = [&](int slot) {
-    if (tid == 0) {
+    if (tid == 0 && a.phases) {  // phase timers only when the caller asked for them
       const uint64_t t = globaltimer_ns();
       ph[slot] += double(t - t_last) * 1e-9;
       t_last = t;
     }
   };
   if (tid == 0) {
-    t_last = globaltimer_ns();
+    if (a.phases) t_last = globaltimer_ns();
     iflag[0] = 0;
     iflag[1] = -1;
     for (int q = 0; q < 4 * NVB; q += 2 * NVB)

@@ -1504,14 +1504,15 @@ __global__ void __launch_bounds__(NT, 1) lse_reg_kernel(TileArgs a) {
     for (int i = tid; i < p; i += NT) y2[i] = float(rinit[m + i]);
     __syncthreads();
     if (w == 0) {
+      // y2 = R^-1 d, then T12 y2 -- both beside the Z group's four WY blocks
       trsv_up<float>(M, ld, m, n - p, p, rinvRf, y2, l);
+      __syncwarp();
+      gemv_rows<float, false>(M, ld, 0, k, k, p, y2, t4, l, 32);
     } else if (w >= NW - ZG) {
       z_apply_mw<float>(M, ld, kz, m, TZ, true, c, partZf, wscf, Grp{w - (NW - ZG), ZG, l, 1});  // c = Z^T b
     }
     __syncthreads();
     if (iflag[0]) goto finish;
-    gemv_rows<float, false>(M, ld, 0, k, k, p, y2, t4, tid, NT);
-    __syncthreads();
     if (w < QG) {
       const Grp g{w, QG, l, 2};
       if (w == 0) {

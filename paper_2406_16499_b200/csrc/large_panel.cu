@@ -871,17 +871,30 @@ cudaError_t panel_factor(T* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb
   cudaError_t e;
   static const bool smem_panel = getenv("MLSB_PANEL_SMEM") != nullptr;  // A/B comparisons
   if constexpr (std::is_same<T, float>::value) {
-    // register-resident rows: 128 threads x 4 rows per CTA (one warp per SM
-    // sub-partition) while 16 CTAs hold the panel, else 512 x 2
+    // register-resident rows: 256 threads x 2 rows per CTA while 16 CTAs hold
+    // the panel, else 512 x 2
     if (L <= PCL * 512 * 2 && !smem_panel) {
       const bool small = L <= PCL * 128 * 4;
+      // 256 threads x 2 rows per CTA: two warps per scheduler hide each other's
+      // latency (ncu: the 128 x 4 form runs at IPC 0.69 with one warp per
+      // scheduler, ~760 instructions per warp and reflector at ~5.8 cycles
+      // each).  Measured at 8192 x 32: 61.8 us (128 x 4), 57.6 us (256 x 2),
+      // 68.5 us (512 x 1); C3 factorization 24.9 / 23.4 / 24.9 ms.
+      // MLSB_PANEL_256=0 / 2 select the other two forms (A/B).
+      static const int pvar = getenv("MLSB_PANEL_256") ? atoi(getenv("MLSB_PANEL_256")) : 1;
+      const bool p256 = pvar == 1, p512 = pvar == 2;
       const int per = small ? 128 * 4 : 512 * 2;
       const int ncl = std::min(PCL, (L + per - 1) / per);
       a.ncl = ncl;
       a.rc = (L + ncl - 1) / ncl;
-      auto kern = small ? panel_reg_kernel<4, 128> : panel_reg_kernel<2, 512>;
+      auto kern = small ? (p256 ? panel_reg_kernel<2, 256> : (p512 ? panel_reg_kernel<1, 512> : panel_reg_kernel<4, 128>))
+                        : panel_reg_kernel<2, 512>;
       static bool attr_reg = false;
       if (!attr_reg) {
+        if ((e = cudaFuncSetAttribute(panel_reg_kernel<2, 256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)))
+          return e;
+        if ((e = cudaFuncSetAttribute(panel_reg_kernel<1, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)))
+          return e;
         if ((e = cudaFuncSetAttribute(panel_reg_kernel<4, 128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)))
           return e;
         if ((e = cudaFuncSetAttribute(panel_reg_kernel<2, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)))
@@ -889,7 +902,7 @@ cudaError_t panel_factor(T* M, int64_t ld, int64_t r0, int64_t c0, int L, int nb
         attr_reg = true;
       }
       cfg.gridDim = dim3(ncl);
-      cfg.blockDim = dim3(small ? 128 : 512);
+      cfg.blockDim = dim3(small ? (p256 ? 256 : (p512 ? 512 : 128)) : 512);
       cfg.dynamicSmemBytes = 0;
       attr[0].val.clusterDim.x = ncl;
       return cudaLaunchKernelEx(&cfg, kern, a);
